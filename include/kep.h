@@ -1,0 +1,193 @@
+/*
+ * kep.h — C ABI of the B200-native nu_sigma(A, B) engine (arXiv 1710.05134).
+ *
+ * What it computes
+ * ----------------
+ * nu_sigma(A, B) = #{ i : lambda_i < sigma } for the symmetric-definite pencil
+ * A x = lambda B x (Eq. 1.1; PAPER.md:45 definition of nu), via
+ * a sparse symmetric-indefinite factorisation
+ *     L D L^T = P Q (A - sigma B) Q^T P^T          (Alg. 1' line 3)
+ * and Sylvester's law of inertia, nu = nu_0(D, I).
+ * Q is a fill-reducing ordering computed once per sparsity pattern and recycled
+ * for every shift (§3.3); P is the Bunch-Kaufman stability
+ * permutation, chosen per shift inside each front with delayed
+ * pivots (reading R1).  D has 1x1 and 2x2 blocks; a 2x2 block is
+ * classified by the sign of its determinant (reading R2).
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ * - Real fp64 values, 0-based indices.  Matrices are given as the LOWER
+ *   triangle (row >= col) in compressed sparse column form of the UNION
+ *   pattern of A and B: colptr[n+1] (int64), rowidx
+ *   (int32, sorted within each column, diagonal present).  A and B value
+ *   arrays are aligned with rowidx; explicit zeros are allowed.
+ * - Ownership: every pointer argument is owned by the caller and may be freed
+ *   when the call returns; the library copies what it needs.  A kep_ctx owns
+ *   all device memory it allocates; kep_destroy releases it.
+ * - Errors: every function returns a kep_status and never aborts or throws
+ *   across the ABI.  Outputs are written only on KEP_OK, except that
+ *   kep_inertia fills `info` also on KEP_ESINGULAR.  kep_last_error gives a
+ *   human-readable message for the last failing call on a context.
+ * - Threading: one ctx = one CUDA device + one stream; calls on one ctx must be
+ *   serialised by the caller; distinct ctxs may be used concurrently.
+ * - Host pointers unless the name says `_dev`.
+ */
+#ifndef KEP_H
+#define KEP_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#if defined(__GNUC__)
+#define KEP_API __attribute__((visibility("default")))
+#else
+#define KEP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KEP_OK = 0,
+    KEP_EINVAL = 1,       /* bad argument (null pointer, n < 0, unsorted / upper entries, ...) */
+    KEP_EPATTERN = 2,     /* values do not match the analysed pattern */
+    KEP_ESINGULAR = 3,    /* some |pivot| <= tau_sing * max|A - sigma B|: sigma is
+                             (numerically) an eigenvalue; perturb sigma and retry */
+    KEP_ENOTSPD = 4,      /* reserved: B failed an all-positive-pivot check */
+    KEP_ENOMEM = 5,       /* host or device allocation failed */
+    KEP_ECUDA = 6,        /* a CUDA runtime error (message in kep_last_error) */
+    KEP_EBREAKDOWN = 7,   /* reserved (Lanczos breakdown, NEXT f2/f3) */
+    KEP_ENOCONV = 8,      /* reserved (NEXT f2) */
+    KEP_ECLUSTER = 9,     /* reserved status, not an error */
+    KEP_ENODEVICE = 10    /* no usable CUDA device */
+} kep_status;
+
+typedef enum {
+    KEP_ORDER_AUTO = 0,     /* METIS nested dissection (default) */
+    KEP_ORDER_METIS = 1,    /* METIS_NodeND on the supervariable quotient graph */
+    KEP_ORDER_NATURAL = 2,  /* identity (testing) */
+    KEP_ORDER_USER = 3      /* caller-supplied permutation `user_perm` */
+} kep_ordering;
+
+typedef struct {
+    kep_ordering ordering;      /* default KEP_ORDER_AUTO */
+    const int64_t* user_perm;   /* KEP_ORDER_USER: user_perm[i] = dof placed i-th; length n */
+    int32_t amalgamate;         /* relaxed supernode amalgamation on (1, default) / off (0) */
+    int32_t nrelax;             /* merge child into parent if merged pivot count <= nrelax (default 16) */
+    double relax_frac;          /* ... or if the added zeros are <= relax_frac of the merged L (default 0.05) */
+    double pivot_u;             /* threshold for delayed pivots, u in (0, 0.5]; default 0.01 (DESIGN R1) */
+    double tau_sing;            /* singularity tolerance relative to max|A - sigma B|; default 1e-14 */
+    int32_t delay_slack;        /* initial per-front slack (columns) for delayed pivots; default 16 */
+    int32_t max_batch;          /* max shifts factorised concurrently on the device; default 16 */
+    int32_t device;             /* CUDA device ordinal; -1 = current (default) */
+    void* stream;               /* cudaStream_t to run on; NULL = a stream owned by the ctx */
+    int32_t kernel_variant;     /* 0 = default (fastest), 1 = reference unblocked kernels (testing) */
+    int32_t profile;            /* 1 = time every kernel class with CUDA events on the ctx stream */
+} kep_opts;
+
+/* Kernel classes for kep_profile (rows of SURVEY.md §8(a)). */
+enum { KEP_K_ASSEMBLE = 0,   /* a1 + a2: assembly + extend-add */
+       KEP_K_PANEL = 1,      /* a3 + a5: blocked Bunch-Kaufman panel (FS columns) */
+       KEP_K_REF = 2,        /* a3 + a4 + a5: reference unblocked front factorisation */
+       KEP_K_SCHUR = 3,      /* a4: DMMA contribution-block update */
+       KEP_K_NCLASS = 4 };
+
+typedef struct {
+    double ms[KEP_K_NCLASS];          /* summed CUDA-event time per class (profile = 1 only) */
+    int64_t launches[KEP_K_NCLASS];   /* kernel launches per class (always counted) */
+    double schur_flops;               /* algorithmic a4 flops p c (c + 1) summed over the fronts
+                                         whose Schur update ran in KEP_K_SCHUR launches */
+    double factor_flops;              /* algorithmic flops of all factorisations run (kep_analysis_info.flops each) */
+    int64_t shifts;                   /* shifts factorised */
+    int64_t other_launches;           /* bookkeeping kernels (stat reset) */
+} kep_profile;
+
+typedef struct {
+    int64_t n_neg, n_zero, n_pos;   /* inertia of D; nu = n_neg */
+    int64_t n_2x2;                  /* number of 2x2 pivot blocks */
+    int64_t n_delayed;              /* columns delayed to a parent front (sum over fronts) */
+    double min_abs_pivot;           /* min over blocks of the smallest |eigenvalue| */
+    double max_abs_entry;           /* max |a_ij - sigma b_ij| */
+} kep_inertia_info;
+
+typedef struct {
+    int64_t n;                  /* matrix order */
+    int64_t nnz_lower;          /* stored lower entries of the union pattern */
+    int64_t n_supervariables;   /* dof groups with identical structure (atoms) */
+    int64_t n_fronts;           /* supernodes after amalgamation */
+    int64_t n_levels;           /* elimination-tree levels (leaves = 0) */
+    int64_t max_front;          /* largest front order f (no delays) */
+    int64_t max_level_width;    /* largest number of fronts in one level */
+    int64_t nzf;                /* entries of L (incl. diagonal) on fundamental supernodes (#nzf) */
+    int64_t nzf_exec;           /* entries of L on the amalgamated fronts */
+    double flops;               /* algorithmic factor flops per shift, fundamental supernodes, no delays */
+    double flops_exec;          /* flops executed on the amalgamated fronts (no delays) */
+    double flops_schur;         /* part of flops_exec in the contribution-block update (row a4) */
+    int64_t sum_cb;             /* sum over fronts of lower CB entries c(c+1)/2 */
+    int64_t arena_bytes;        /* device front arena per shift */
+    int32_t delay_slack;        /* current per-front slack */
+    int32_t batch;              /* shifts factorised concurrently */
+} kep_analysis_info;
+
+typedef struct kep_ctx kep_ctx;
+
+/* Fill `opts` with the defaults listed above. */
+KEP_API void kep_default_opts(kep_opts* opts);
+
+/* Symbolic analysis of the union pattern (untimed setup, once per pattern;
+ * PAPER.md:61, :400-403).  Validates the lower CSC, groups
+ * identical-structure dofs into supervariables, orders the quotient graph with
+ * nested dissection, builds the elimination tree, supernodes, front structures,
+ * assembly and extend-add maps and the level schedule, and copies the static
+ * maps to the device.  opts may be NULL (defaults).
+ * Errors: KEP_EINVAL (malformed CSC, n <= 0, entry above the diagonal,
+ * missing diagonal, front larger than 65535), KEP_ENOMEM, KEP_ECUDA,
+ * KEP_ENODEVICE. */
+KEP_API kep_status kep_analyze(int64_t n, const int64_t* colptr, const int32_t* rowidx,
+                       const kep_opts* opts, kep_ctx** out);
+
+/* Values of A and B aligned with the analysed rowidx (nnz_lower each, host).
+ * Copied to the device in assembly order.  Must precede kep_inertia. */
+KEP_API kep_status kep_set_values(kep_ctx* ctx, const double* a, const double* b);
+
+/* Same, from device pointers (nnz_lower doubles each, on the ctx device). */
+KEP_API kep_status kep_set_values_dev(kep_ctx* ctx, const double* a_dev, const double* b_dev);
+
+/* nu_sigma(A, B) for one shift (the timed hot path: assembly, extend-add,
+ * Bunch-Kaufman partial LDL^T with delayed pivots, Schur update, inertia).
+ * Returns KEP_OK and *nu, or KEP_ESINGULAR (info filled, *nu untouched).
+ * info may be NULL. */
+KEP_API kep_status kep_inertia(kep_ctx* ctx, double sigma, int64_t* nu, kep_inertia_info* info);
+
+/* nu for m shifts (batched on the device, max_batch at a time).  nus[i] is
+ * written when per_shift[i] == KEP_OK.  infos may be NULL.  Returns KEP_OK if
+ * the call ran (individual shifts may be KEP_ESINGULAR), else the error. */
+KEP_API kep_status kep_inertia_many(kep_ctx* ctx, int32_t m, const double* sigmas, int64_t* nus,
+                            kep_status* per_shift, kep_inertia_info* infos);
+
+/* Analysis statistics (sizes, #nzf, flops per shift, memory). */
+KEP_API kep_status kep_get_analysis(const kep_ctx* ctx, kep_analysis_info* info);
+
+/* Accumulated kernel statistics since the last reset (see kep_opts.profile). */
+KEP_API kep_status kep_get_profile(const kep_ctx* ctx, kep_profile* prof);
+KEP_API kep_status kep_reset_profile(kep_ctx* ctx);
+
+/* The fill-reducing permutation chosen: perm[i] = dof placed i-th (length n). */
+KEP_API kep_status kep_get_perm(const kep_ctx* ctx, int64_t* perm);
+
+/* Supernode partition and assembly tree (testing / diagnostics):
+ * first[s] .. first[s+1]-1 are the pivot positions of front s (n_fronts+1
+ * entries), parent[s] = parent front or -1, front_order[s] = f_s. */
+KEP_API kep_status kep_get_fronts(const kep_ctx* ctx, int64_t* first, int64_t* parent, int64_t* front_order);
+
+KEP_API void kep_destroy(kep_ctx* ctx);
+KEP_API const char* kep_status_string(kep_status s);
+KEP_API const char* kep_last_error(const kep_ctx* ctx);
+/* Library version string, e.g. "kep 0.1 sm_100a". */
+KEP_API const char* kep_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KEP_H */

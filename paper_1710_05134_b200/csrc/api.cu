@@ -1,0 +1,549 @@
+// api.cu — the C ABI (include/kep.h): context, device memory, shift batches.
+//
+// Boundary of SURVEY.md §8(b): kep_analyze (pattern-only setup, untimed),
+// kep_set_values, kep_inertia / kep_inertia_many (the timed hot path).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/kep.h"
+#include "device.cuh"
+#include "symbolic.h"
+
+using kep::DevPlan;
+using kep::ShiftStat;
+using kep::Symbolic;
+
+struct kep_ctx {
+    Symbolic sym;
+    kep_opts opts;
+    std::string err;
+    bool have_device = false;
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool values_set = false;
+    int batch_cap = 1;
+    // device arrays (static)
+    int32_t *d_forder = nullptr, *d_npiv = nullptr, *d_ncb = nullptr, *d_cap = nullptr;
+    int32_t *d_child_ptr = nullptr, *d_child_list = nullptr, *d_level_fronts = nullptr;
+    int64_t *d_arena_off = nullptr, *d_asm_ptr = nullptr, *d_asm_src = nullptr, *d_rmap_ptr = nullptr;
+    uint32_t* d_asm_rc = nullptr;
+    int32_t* d_rmap = nullptr;
+    double *d_a = nullptr, *d_b = nullptr;
+    // batch state
+    double* d_arena = nullptr;
+    size_t arena_alloc_doubles = 0;
+    int32_t *d_nd_in = nullptr, *d_nd_out = nullptr, *d_doff = nullptr;
+    ShiftStat* d_stats = nullptr;
+    double* d_sigma = nullptr;
+    std::vector<ShiftStat> h_stats;
+    // per-level launch lists: fast (panel + Schur) and reference fronts
+    int32_t* d_lists = nullptr;                 // [fast fronts of all levels | ref fronts of all levels]
+    int4* d_items = nullptr;                    // Schur tiles (front, I, J, 0)
+    std::vector<int64_t> fast_off, fast_cnt, ref_off, ref_cnt, item_off, item_cnt;
+    int max_fast_cap = 0;
+    std::vector<double> item_flops;             // per level: algorithmic a4 flops of its fast fronts
+    // profiling
+    kep_profile prof;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<int> ev_class;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+kep_status fail(kep_ctx* c, kep_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    g_err = msg;
+    return s;
+}
+
+#define KEP_CUDA(ctx, call)                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? KEP_ENOMEM : KEP_ECUDA,        \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+    } while (0)
+
+template <class T>
+cudaError_t upload(T** dptr, const std::vector<T>& h) {
+    size_t bytes = std::max<size_t>(h.size(), 1) * sizeof(T);
+    cudaError_t e = cudaMalloc((void**)dptr, bytes);
+    if (e != cudaSuccess) return e;
+    if (!h.empty()) e = cudaMemcpy(*dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+void free_batch(kep_ctx* c) {
+    cudaFree(c->d_arena); c->d_arena = nullptr; c->arena_alloc_doubles = 0;
+    cudaFree(c->d_nd_in); c->d_nd_in = nullptr;
+    cudaFree(c->d_nd_out); c->d_nd_out = nullptr;
+    cudaFree(c->d_doff); c->d_doff = nullptr;
+    cudaFree(c->d_stats); c->d_stats = nullptr;
+    cudaFree(c->d_sigma); c->d_sigma = nullptr;
+}
+
+// (Re)allocate the per-batch state for the current memory plan.
+kep_status alloc_batch(kep_ctx* c) {
+    free_batch(c);
+    size_t freeb = 0, totalb = 0;
+    KEP_CUDA(c, cudaMemGetInfo(&freeb, &totalb));
+    const size_t per_shift = (size_t)c->sym.arena_doubles * sizeof(double);
+    int cap = std::max(1, c->opts.max_batch);
+    const size_t budget = (size_t)(0.85 * (double)freeb);
+    while (cap > 1 && per_shift * (size_t)cap > budget) cap--;
+    if (per_shift > budget) return fail(c, KEP_ENOMEM, "front arena of one shift does not fit in device memory");
+    c->batch_cap = cap;
+    c->arena_alloc_doubles = (size_t)c->sym.arena_doubles * cap;
+    KEP_CUDA(c, cudaMalloc(&c->d_arena, c->arena_alloc_doubles * sizeof(double)));
+    const size_t nfb = (size_t)std::max<int64_t>(c->sym.nf, 1) * cap * sizeof(int32_t);
+    KEP_CUDA(c, cudaMalloc(&c->d_nd_in, nfb));
+    KEP_CUDA(c, cudaMalloc(&c->d_nd_out, nfb));
+    KEP_CUDA(c, cudaMalloc(&c->d_doff, nfb));
+    KEP_CUDA(c, cudaMalloc(&c->d_stats, sizeof(ShiftStat) * cap));
+    KEP_CUDA(c, cudaMalloc(&c->d_sigma, sizeof(double) * cap));
+    c->h_stats.resize(cap);
+    return KEP_OK;
+}
+
+// Split every level into fronts for the blocked panel kernel (+ DMMA Schur
+// tiles) and fronts for the reference kernel; build the Schur work items.
+kep_status build_lists(kep_ctx* c) {
+    const Symbolic& S = c->sym;
+    const int nl = (int)S.level_ptr.size() - 1;
+    const int lim = kep::panel_max_front();
+    const bool use_fast = c->opts.kernel_variant == 0;
+    std::vector<int32_t> fast, ref;
+    std::vector<int4> items;
+    c->fast_off.assign(nl, 0); c->fast_cnt.assign(nl, 0);
+    c->ref_off.assign(nl, 0); c->ref_cnt.assign(nl, 0);
+    c->item_off.assign(nl, 0); c->item_cnt.assign(nl, 0);
+    c->max_fast_cap = 0;
+    for (int L = 0; L < nl; ++L) {
+        c->fast_off[L] = (int64_t)fast.size();
+        c->ref_off[L] = (int64_t)ref.size();
+        c->item_off[L] = (int64_t)items.size();
+        for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
+            const int s = S.level_fronts[k];
+            if (use_fast && S.capacity[s] <= lim) {
+                fast.push_back(s);
+                c->max_fast_cap = std::max(c->max_fast_cap, (int)S.capacity[s]);
+                const int nt = (S.ncb[s] + 63) / 64;
+                for (int I = 0; I < nt; ++I)
+                    for (int J = 0; J <= I; ++J) items.push_back(make_int4(s, I, J, 0));
+            } else {
+                ref.push_back(s);
+            }
+        }
+        c->fast_cnt[L] = (int64_t)fast.size() - c->fast_off[L];
+        c->ref_cnt[L] = (int64_t)ref.size() - c->ref_off[L];
+        c->item_cnt[L] = (int64_t)items.size() - c->item_off[L];
+    }
+    c->item_flops.assign(nl, 0.0);
+    for (int L = 0; L < nl; ++L)
+        for (int64_t k = c->fast_off[L]; k < c->fast_off[L] + c->fast_cnt[L]; ++k) {
+            const int s = fast[k];
+            c->item_flops[L] += (double)S.npiv[s] * (double)S.ncb[s] * (double)(S.ncb[s] + 1);
+        }
+    std::vector<int32_t> lists(fast);
+    lists.insert(lists.end(), ref.begin(), ref.end());
+    const int64_t nfast = (int64_t)fast.size();
+    for (int L = 0; L < nl; ++L) c->ref_off[L] += nfast;
+    cudaFree(c->d_lists); c->d_lists = nullptr;
+    cudaFree(c->d_items); c->d_items = nullptr;
+    KEP_CUDA(c, upload(&c->d_lists, lists));
+    KEP_CUDA(c, upload(&c->d_items, items));
+    return KEP_OK;
+}
+
+kep_status upload_plan(kep_ctx* c) {
+    const Symbolic& S = c->sym;
+    KEP_CUDA(c, upload(&c->d_forder, S.forder));
+    KEP_CUDA(c, upload(&c->d_npiv, S.npiv));
+    KEP_CUDA(c, upload(&c->d_ncb, S.ncb));
+    KEP_CUDA(c, upload(&c->d_cap, S.capacity));
+    KEP_CUDA(c, upload(&c->d_child_ptr, S.child_ptr));
+    KEP_CUDA(c, upload(&c->d_child_list, S.child_list));
+    KEP_CUDA(c, upload(&c->d_level_fronts, S.level_fronts));
+    KEP_CUDA(c, upload(&c->d_arena_off, S.arena_off));
+    KEP_CUDA(c, upload(&c->d_asm_ptr, S.asm_ptr));
+    KEP_CUDA(c, upload(&c->d_asm_src, S.asm_src));
+    KEP_CUDA(c, upload(&c->d_asm_rc, S.asm_rc));
+    KEP_CUDA(c, upload(&c->d_rmap_ptr, S.rmap_ptr));
+    KEP_CUDA(c, upload(&c->d_rmap, S.rmap));
+    KEP_CUDA(c, cudaMalloc(&c->d_a, std::max<int64_t>(S.nnz, 1) * sizeof(double)));
+    KEP_CUDA(c, cudaMalloc(&c->d_b, std::max<int64_t>(S.nnz, 1) * sizeof(double)));
+    kep_status r = build_lists(c);
+    if (r != KEP_OK) return r;
+    return alloc_batch(c);
+}
+
+// after a slack overflow: larger slack, new plan, re-upload the plan arrays that changed
+kep_status replan(kep_ctx* c, int slack) {
+    kep::plan_memory(c->sym, slack);
+    cudaFree(c->d_cap);
+    cudaFree(c->d_arena_off);
+    c->d_cap = nullptr;
+    c->d_arena_off = nullptr;
+    KEP_CUDA(c, upload(&c->d_cap, c->sym.capacity));
+    KEP_CUDA(c, upload(&c->d_arena_off, c->sym.arena_off));
+    kep_status r = build_lists(c);
+    if (r != KEP_OK) return r;
+    return alloc_batch(c);
+}
+
+DevPlan make_plan(kep_ctx* c) {
+    DevPlan P;
+    P.nf = (int32_t)c->sym.nf;
+    P.forder = c->d_forder;
+    P.npiv = c->d_npiv;
+    P.ncb = c->d_ncb;
+    P.cap = c->d_cap;
+    P.child_ptr = c->d_child_ptr;
+    P.child_list = c->d_child_list;
+    P.level_fronts = c->d_level_fronts;
+    P.arena_off = c->d_arena_off;
+    P.asm_ptr = c->d_asm_ptr;
+    P.asm_rc = c->d_asm_rc;
+    P.a = c->d_a;
+    P.b = c->d_b;
+    P.rmap_ptr = c->d_rmap_ptr;
+    P.rmap = c->d_rmap;
+    P.arena = c->d_arena;
+    P.arena_stride = c->sym.arena_doubles;
+    P.nd_in = c->d_nd_in;
+    P.nd_out = c->d_nd_out;
+    P.doff = c->d_doff;
+    P.stats = c->d_stats;
+    P.sigma = c->d_sigma;
+    P.u = c->opts.pivot_u;
+    return P;
+}
+
+// One batch of `m` shifts through every level.  Fills c->h_stats[0..m).
+kep_status run_batch(kep_ctx* c, int m, const double* sigmas) {
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        if (m > c->batch_cap) return fail(c, KEP_EINVAL, "internal: batch larger than capacity");
+        KEP_CUDA(c, cudaMemcpyAsync(c->d_sigma, sigmas, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+        kep::launch_reset_stats(c->d_stats, m, c->stream);
+        c->prof.other_launches += 1;
+        DevPlan P = make_plan(c);
+        const Symbolic& S = c->sym;
+        const int nl = (int)S.level_ptr.size() - 1;
+        const bool prof = c->opts.profile != 0;
+        size_t nev = 0;
+        auto mark = [&](int cls, bool begin) {
+            if (!prof) return;
+            if (nev >= c->ev_pool.size()) {
+                cudaEvent_t ev;
+                cudaEventCreate(&ev);
+                c->ev_pool.push_back(ev);
+                c->ev_class.push_back(0);
+            }
+            cudaEventRecord(c->ev_pool[nev], c->stream);
+            c->ev_class[nev] = begin ? cls : -1;
+            ++nev;
+        };
+        for (int L = 0; L < nl; ++L) {
+            const int b = S.level_ptr[L], nfl = S.level_ptr[L + 1] - b;
+            mark(KEP_K_ASSEMBLE, true);
+            kep::launch_assemble(P, b, nfl, m, c->stream);
+            mark(KEP_K_ASSEMBLE, false);
+            c->prof.launches[KEP_K_ASSEMBLE]++;
+            if (c->fast_cnt[L]) {
+                mark(KEP_K_PANEL, true);
+                kep::launch_panel(P, c->d_lists + c->fast_off[L], (int)c->fast_cnt[L], m, c->max_fast_cap, c->stream);
+                mark(KEP_K_PANEL, false);
+                c->prof.launches[KEP_K_PANEL]++;
+            }
+            if (c->ref_cnt[L]) {
+                mark(KEP_K_REF, true);
+                kep::launch_factor_list(P, c->d_lists + c->ref_off[L], (int)c->ref_cnt[L], m, c->stream);
+                mark(KEP_K_REF, false);
+                c->prof.launches[KEP_K_REF]++;
+            }
+            if (c->item_cnt[L]) {
+                mark(KEP_K_SCHUR, true);
+                kep::launch_schur(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
+                mark(KEP_K_SCHUR, false);
+                c->prof.launches[KEP_K_SCHUR]++;
+                c->prof.schur_flops += c->item_flops[L] * m;
+            }
+        }
+        KEP_CUDA(c, cudaGetLastError());
+        KEP_CUDA(c, cudaMemcpyAsync(c->h_stats.data(), c->d_stats, sizeof(ShiftStat) * m, cudaMemcpyDeviceToHost, c->stream));
+        KEP_CUDA(c, cudaStreamSynchronize(c->stream));
+        for (size_t x = 0; x + 1 < nev; x += 2) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c->ev_pool[x], c->ev_pool[x + 1]);
+            c->prof.ms[c->ev_class[x]] += ms;
+        }
+        c->prof.shifts += m;
+        c->prof.factor_flops += c->sym.flops * m;
+        int need = 0;
+        bool over = false;
+        for (int i = 0; i < m; ++i)
+            if (c->h_stats[i].flags & kep::FLAG_OVERFLOW) { over = true; need = std::max(need, c->h_stats[i].need_slack); }
+        if (!over) return KEP_OK;
+        int slack = std::max(2 * c->sym.slack, need + 8);
+        kep_status r = replan(c, slack);
+        if (r != KEP_OK) return r;
+        m = std::min(m, c->batch_cap);
+    }
+    return fail(c, KEP_ENOMEM, "delayed-pivot slack kept overflowing");
+}
+
+double bits_to_double(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, sizeof(d));
+    return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+void kep_default_opts(kep_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->ordering = KEP_ORDER_AUTO;
+    o->user_perm = nullptr;
+    o->amalgamate = 1;
+    o->nrelax = 16;
+    o->relax_frac = 0.05;
+    o->pivot_u = 0.01;
+    o->tau_sing = 1e-14;
+    o->delay_slack = 16;
+    o->max_batch = 16;
+    o->device = -1;
+    o->stream = nullptr;
+    o->kernel_variant = 0;
+    o->profile = 0;
+}
+
+const char* kep_version(void) { return "kep 0.1 sm_100a"; }
+
+const char* kep_status_string(kep_status s) {
+    switch (s) {
+        case KEP_OK: return "KEP_OK";
+        case KEP_EINVAL: return "KEP_EINVAL";
+        case KEP_EPATTERN: return "KEP_EPATTERN";
+        case KEP_ESINGULAR: return "KEP_ESINGULAR";
+        case KEP_ENOTSPD: return "KEP_ENOTSPD";
+        case KEP_ENOMEM: return "KEP_ENOMEM";
+        case KEP_ECUDA: return "KEP_ECUDA";
+        case KEP_EBREAKDOWN: return "KEP_EBREAKDOWN";
+        case KEP_ENOCONV: return "KEP_ENOCONV";
+        case KEP_ECLUSTER: return "KEP_ECLUSTER";
+        case KEP_ENODEVICE: return "KEP_ENODEVICE";
+    }
+    return "KEP_UNKNOWN";
+}
+
+const char* kep_last_error(const kep_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+kep_status kep_analyze(int64_t n, const int64_t* colptr, const int32_t* rowidx, const kep_opts* opts, kep_ctx** out) {
+    if (!out) return fail(nullptr, KEP_EINVAL, "out is NULL");
+    *out = nullptr;
+    kep_ctx* c = new (std::nothrow) kep_ctx();
+    if (!c) return fail(nullptr, KEP_ENOMEM, "host allocation failed");
+    std::memset(&c->prof, 0, sizeof(c->prof));
+    if (opts) c->opts = *opts; else kep_default_opts(&c->opts);
+    if (c->opts.pivot_u <= 0.0 || c->opts.pivot_u > 0.5) { delete c; return fail(nullptr, KEP_EINVAL, "pivot_u must be in (0, 0.5]"); }
+    if (c->opts.max_batch < 1) c->opts.max_batch = 1;
+    if (c->opts.delay_slack < 0) c->opts.delay_slack = 0;
+    kep::SymbolicOptions so;
+    so.ordering = (int)c->opts.ordering;
+    so.user_perm = c->opts.user_perm;
+    so.amalgamate = c->opts.amalgamate != 0;
+    so.nrelax = c->opts.nrelax;
+    so.relax_frac = c->opts.relax_frac;
+    so.delay_slack = c->opts.delay_slack;
+    std::string msg;
+    try {
+        msg = kep::analyze(n, colptr, rowidx, so, c->sym);
+    } catch (const std::bad_alloc&) {
+        delete c;
+        return fail(nullptr, KEP_ENOMEM, "host allocation failed during analysis");
+    } catch (const std::exception& e) {
+        delete c;
+        return fail(nullptr, KEP_EINVAL, e.what());
+    }
+    if (!msg.empty()) { delete c; return fail(nullptr, KEP_EINVAL, msg); }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        c->have_device = false;           // symbolic queries still work (CPU-only hosts)
+        *out = c;
+        return KEP_OK;
+    }
+    c->device = c->opts.device >= 0 ? c->opts.device : 0;
+    if (c->opts.device < 0) cudaGetDevice(&c->device);
+    if (cudaSetDevice(c->device) != cudaSuccess) { delete c; return fail(nullptr, KEP_ENODEVICE, "cudaSetDevice failed"); }
+    c->have_device = true;
+    if (c->opts.stream) c->stream = (cudaStream_t)c->opts.stream;
+    else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { delete c; return fail(nullptr, KEP_ECUDA, "stream creation failed"); }
+        c->own_stream = true;
+    }
+    kep_status st = upload_plan(c);
+    if (st != KEP_OK) { std::string m = c->err; kep_destroy(c); return fail(nullptr, st, m); }
+    *out = c;
+    return KEP_OK;
+}
+
+kep_status kep_set_values_dev(kep_ctx* c, const double* a_dev, const double* b_dev) {
+    if (!c || !a_dev || !b_dev) return fail(c, KEP_EINVAL, "null argument");
+    if (!c->have_device) return fail(c, KEP_ENODEVICE, "no CUDA device");
+    KEP_CUDA(c, cudaSetDevice(c->device));
+    kep::launch_gather(a_dev, c->d_asm_src, c->d_a, c->sym.nnz, c->stream);
+    kep::launch_gather(b_dev, c->d_asm_src, c->d_b, c->sym.nnz, c->stream);
+    KEP_CUDA(c, cudaGetLastError());
+    KEP_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->values_set = true;
+    return KEP_OK;
+}
+
+kep_status kep_set_values(kep_ctx* c, const double* a, const double* b) {
+    if (!c || !a || !b) return fail(c, KEP_EINVAL, "null argument");
+    if (!c->have_device) return fail(c, KEP_ENODEVICE, "no CUDA device");
+    KEP_CUDA(c, cudaSetDevice(c->device));
+    const size_t bytes = (size_t)c->sym.nnz * sizeof(double);
+    double *ta = nullptr, *tb = nullptr;
+    KEP_CUDA(c, cudaMalloc(&ta, std::max<size_t>(bytes, 8)));
+    cudaError_t e = cudaMalloc(&tb, std::max<size_t>(bytes, 8));
+    if (e != cudaSuccess) { cudaFree(ta); return fail(c, KEP_ENOMEM, "cudaMalloc failed"); }
+    e = cudaMemcpyAsync(ta, a, bytes, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tb, b, bytes, cudaMemcpyHostToDevice, c->stream);
+    kep_status st = KEP_OK;
+    if (e != cudaSuccess) st = fail(c, KEP_ECUDA, cudaGetErrorString(e));
+    else st = kep_set_values_dev(c, ta, tb);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(ta);
+    cudaFree(tb);
+    return st;
+}
+
+kep_status kep_inertia_many(kep_ctx* c, int32_t m, const double* sigmas, int64_t* nus, kep_status* per_shift,
+                            kep_inertia_info* infos) {
+    if (!c || (m > 0 && (!sigmas || !nus || !per_shift))) return fail(c, KEP_EINVAL, "null argument");
+    if (m < 0) return fail(c, KEP_EINVAL, "m < 0");
+    if (!c->have_device) return fail(c, KEP_ENODEVICE, "no CUDA device");
+    if (!c->values_set) return fail(c, KEP_EINVAL, "kep_set_values must precede kep_inertia");
+    KEP_CUDA(c, cudaSetDevice(c->device));
+    int done = 0;
+    while (done < m) {
+        const int b = std::min(m - done, c->batch_cap);
+        kep_status st = run_batch(c, b, sigmas + done);
+        if (st != KEP_OK) return st;
+        const int got = std::min(b, c->batch_cap);     // a replan may shrink the batch
+        for (int i = 0; i < got; ++i) {
+            const ShiftStat& s = c->h_stats[i];
+            const double minpiv = bits_to_double(s.minpiv_bits);
+            const double smax = bits_to_double(s.smax_bits);
+            const bool singular = s.n_zero > 0 || minpiv <= c->opts.tau_sing * smax;
+            per_shift[done + i] = singular ? KEP_ESINGULAR : KEP_OK;
+            if (!singular) nus[done + i] = (int64_t)s.n_neg;
+            if (infos) {
+                kep_inertia_info& I = infos[done + i];
+                I.n_neg = (int64_t)s.n_neg;
+                I.n_zero = (int64_t)s.n_zero;
+                I.n_pos = (int64_t)s.n_pos;
+                I.n_2x2 = (int64_t)s.n_2x2;
+                I.n_delayed = (int64_t)s.n_delayed;
+                I.min_abs_pivot = minpiv >= DBL_MAX ? 0.0 : minpiv;
+                I.max_abs_entry = smax;
+            }
+        }
+        done += got;
+    }
+    return KEP_OK;
+}
+
+kep_status kep_inertia(kep_ctx* c, double sigma, int64_t* nu, kep_inertia_info* info) {
+    if (!nu) return fail(c, KEP_EINVAL, "nu is NULL");
+    kep_status per = KEP_OK;
+    int64_t v = 0;
+    kep_status st = kep_inertia_many(c, 1, &sigma, &v, &per, info);
+    if (st != KEP_OK) return st;
+    if (per == KEP_OK) *nu = v;
+    return per;
+}
+
+kep_status kep_get_analysis(const kep_ctx* c, kep_analysis_info* I) {
+    if (!c || !I) return KEP_EINVAL;
+    const Symbolic& S = c->sym;
+    I->n = S.n;
+    I->nnz_lower = S.nnz;
+    I->n_supervariables = S.nsv;
+    I->n_fronts = S.nf;
+    I->n_levels = (int64_t)S.level_ptr.size() - 1;
+    I->max_front = S.max_front;
+    I->max_level_width = S.max_level_width;
+    I->nzf = S.nzf;
+    I->nzf_exec = S.nzf_exec;
+    I->flops = S.flops;
+    I->flops_exec = S.flops_exec;
+    I->flops_schur = S.flops_schur;
+    I->sum_cb = S.sum_cb;
+    I->arena_bytes = S.arena_doubles * (int64_t)sizeof(double);
+    I->delay_slack = S.slack;
+    I->batch = c->batch_cap;
+    return KEP_OK;
+}
+
+kep_status kep_get_profile(const kep_ctx* c, kep_profile* p) {
+    if (!c || !p) return KEP_EINVAL;
+    *p = c->prof;
+    return KEP_OK;
+}
+
+kep_status kep_reset_profile(kep_ctx* c) {
+    if (!c) return KEP_EINVAL;
+    std::memset(&c->prof, 0, sizeof(c->prof));
+    return KEP_OK;
+}
+
+kep_status kep_get_perm(const kep_ctx* c, int64_t* perm) {
+    if (!c || !perm) return KEP_EINVAL;
+    std::memcpy(perm, c->sym.perm.data(), sizeof(int64_t) * c->sym.n);
+    return KEP_OK;
+}
+
+kep_status kep_get_fronts(const kep_ctx* c, int64_t* first, int64_t* parent, int64_t* forder) {
+    if (!c) return KEP_EINVAL;
+    const Symbolic& S = c->sym;
+    for (int64_t s = 0; s < S.nf; ++s) {
+        if (first) first[s] = S.piv_first[s];
+        if (parent) parent[s] = S.parent[s];
+        if (forder) forder[s] = S.forder[s];
+    }
+    if (first) first[S.nf] = S.n;
+    return KEP_OK;
+}
+
+void kep_destroy(kep_ctx* c) {
+    if (!c) return;
+    if (c->have_device) {
+        cudaSetDevice(c->device);
+        if (c->stream) cudaStreamSynchronize(c->stream);
+        free_batch(c);
+        void* ptrs[] = {c->d_forder, c->d_npiv, c->d_ncb, c->d_cap, c->d_child_ptr, c->d_child_list,
+                        c->d_level_fronts, c->d_arena_off, c->d_asm_ptr, c->d_asm_src, c->d_rmap_ptr,
+                        c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items};
+        for (void* p : ptrs) cudaFree(p);
+        for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
+        if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    }
+    delete c;
+}
+
+}  // extern "C"

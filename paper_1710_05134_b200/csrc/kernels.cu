@@ -1,0 +1,385 @@
+// kernels.cu — numeric multifrontal LDL^T of A - sigma B, inertia only.
+//
+// Rows a1-a5 of SURVEY.md §8 (BASELINE.json north_star parts (1)-(5)):
+//   a1 assembly of A - sigma B into the fronts of one elimination-tree level
+//   a2 extend-add of the children's contribution blocks (+ delayed columns)
+//   a3 Bunch-Kaufman partial LDL^T of the fully-summed (FS) block with the
+//      threshold test and delayed pivots (reading R1)
+//   a4 Schur-complement update of the contribution block
+//   a5 inertia of D: 1x1 by sign, 2x2 by sign(det) (R2)
+//
+// Front layout (one dense column-major square per front, lower triangle used,
+// leading dimension ld = f_s + nd_s):
+//   [0, p)        own pivots (static order)
+//   [p, p+nd)     columns delayed by the children, children in order
+//   [p+nd, ld)    contribution-block (CB) rows, ascending elimination position
+// After a3 the eliminated pivots sit in [0, e), the columns this front delays
+// in [e, p+nd) and the CB rows are untouched in place, so the trailing block
+// F[e:, e:] is exactly what the parent extend-adds.
+#include <cfloat>
+#include <climits>
+
+#include "device.cuh"
+
+namespace kep {
+
+namespace {
+
+constexpr double kAlpha = 0.6403882032022076;   // (1 + sqrt(17)) / 8, Bunch-Kaufman
+
+struct MaxIdx {
+    double v;
+    int i;
+};
+
+__device__ __forceinline__ MaxIdx better(MaxIdx a, MaxIdx b) {
+    // larger value wins; ties -> lower index (LAPACK idamax semantics)
+    if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+    return a;
+}
+
+template <int NT>
+__device__ MaxIdx block_max_idx(MaxIdx x, MaxIdx* sh) {
+    for (int o = 16; o > 0; o >>= 1) {
+        MaxIdx y;
+        y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+        y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+        x = better(x, y);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        x = l < NT / 32 ? sh[l] : MaxIdx{-1.0, INT_MAX};
+        for (int o = 16; o > 0; o >>= 1) {
+            MaxIdx y;
+            y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+            y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+            x = better(x, y);
+        }
+        if (l == 0) sh[0] = x;
+    }
+    __syncthreads();
+    MaxIdx r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+template <int NT>
+__device__ double block_max(double x, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        x = l < NT / 32 ? sh[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+        if (l == 0) sh[0] = x;
+    }
+    __syncthreads();
+    double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// symmetric access a(i, j) to the lower-stored front
+__device__ __forceinline__ double symget(const double* F, int ld, int i, int j) {
+    return i >= j ? F[i + (size_t)j * ld] : F[j + (size_t)i * ld];
+}
+
+// ---------------------------------------------------------------- a1 + a2
+constexpr int kAsmThreads = 256;
+
+__global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_begin) {
+    const int s = P.level_fronts[lvl_begin + blockIdx.x];
+    const int sh = blockIdx.y;
+    ShiftStat* st = P.stats + sh;
+    double* arena = P.arena + (size_t)sh * P.arena_stride;
+    int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
+    const int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
+    int32_t* doff = P.doff + (size_t)sh * P.nf;
+    __shared__ int s_nd, s_skip;
+    __shared__ double s_red[32];
+    const int c0 = P.child_ptr[s], c1 = P.child_ptr[s + 1];
+    if (threadIdx.x == 0) {
+        int off = 0, bad = 0;
+        for (int q = c0; q < c1; ++q) {
+            const int c = P.child_list[q];
+            const int no = nd_out[c];
+            if (no < 0) bad = 1;
+            doff[c] = off;
+            off += no > 0 ? no : 0;
+        }
+        const int need = P.forder[s] + off;
+        if (need > P.cap[s]) {
+            bad = 1;
+            atomicMax(&st->need_slack, off);
+        }
+        if (bad) atomicOr(&st->flags, FLAG_OVERFLOW);
+        s_skip = bad;
+        s_nd = off;
+        nd_in[s] = bad ? -1 : off;
+    }
+    __syncthreads();
+    if (s_skip) return;
+    const int nd = s_nd, p = P.npiv[s], ld = P.forder[s] + nd;
+    double* F = arena + P.arena_off[s];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAsmThreads / 32;
+    for (int j = warp; j < ld; j += nw)
+        for (int i = j + lane; i < ld; i += 32) F[i + (size_t)j * ld] = 0.0;
+    __syncthreads();
+    const double sigma = P.sigma[sh];
+    double mx = 0.0;
+    for (int64_t k = P.asm_ptr[s] + threadIdx.x; k < P.asm_ptr[s + 1]; k += kAsmThreads) {
+        const uint32_t rc = P.asm_rc[k];
+        const int lr = (int)(rc >> 16), lc = (int)(rc & 0xffffu);
+        const int r = lr < p ? lr : lr + nd;
+        const double v = fma(-sigma, P.b[k], P.a[k]);
+        F[r + (size_t)lc * ld] = v;
+        mx = fmax(mx, fabs(v));
+    }
+    mx = block_max<kAsmThreads>(mx, s_red);
+    if (threadIdx.x == 0) atomic_max_pos_double(&st->smax_bits, mx);
+    // a2: extend-add, children in a fixed order (deterministic, no float atomics)
+    for (int q = c0; q < c1; ++q) {
+        const int c = P.child_list[q];
+        const int ndo = nd_out[c];
+        const int fc = P.forder[c] + nd_in[c];
+        const int mc = ndo + P.ncb[c];
+        const int ec = fc - mc;
+        const double* Fc = arena + P.arena_off[c];
+        const int32_t* rm = P.rmap + P.rmap_ptr[c];
+        const int dof = p + doff[c];
+        for (int j = warp; j < mc; j += nw) {
+            int pj;
+            if (j < ndo) pj = dof + j;
+            else { const int r = rm[j - ndo]; pj = r < p ? r : r + nd; }
+            const double* colc = Fc + (size_t)(ec + j) * fc + ec;
+            for (int i = j + lane; i < mc; i += 32) {
+                int pi;
+                if (i < ndo) pi = dof + i;
+                else { const int r = rm[i - ndo]; pi = r < p ? r : r + nd; }
+                const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
+                F[hi + (size_t)lo * ld] += colc[i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- a3 + a4 + a5 (reference)
+constexpr int kRefThreads = 256;
+
+__device__ void sym_swap(double* F, int ld, int f, int a, int b) {
+    // symmetric row/column interchange of positions a < b (lower storage)
+    if (a == b) return;
+    for (int t = threadIdx.x; t < f; t += blockDim.x) {
+        if (t < a) {
+            double x = F[a + (size_t)t * ld]; F[a + (size_t)t * ld] = F[b + (size_t)t * ld]; F[b + (size_t)t * ld] = x;
+        } else if (t == a) {
+            double x = F[a + (size_t)a * ld]; F[a + (size_t)a * ld] = F[b + (size_t)b * ld]; F[b + (size_t)b * ld] = x;
+        } else if (t < b) {
+            double x = F[t + (size_t)a * ld]; F[t + (size_t)a * ld] = F[b + (size_t)t * ld]; F[b + (size_t)t * ld] = x;
+        } else if (t > b) {
+            double x = F[t + (size_t)a * ld]; F[t + (size_t)a * ld] = F[t + (size_t)b * ld]; F[t + (size_t)b * ld] = x;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int32_t* __restrict__ fronts) {
+    const int s = fronts[blockIdx.x];
+    const int sh = blockIdx.y;
+    ShiftStat* st = P.stats + sh;
+    const int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
+    int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
+    const int nd = nd_in[s];
+    if (nd < 0) {
+        if (threadIdx.x == 0) nd_out[s] = -1;
+        return;
+    }
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const bool root = (c == 0);
+    const double u = P.u;
+    __shared__ MaxIdx s_mi[32];
+    __shared__ double s_red[32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kRefThreads / 32;
+    unsigned long long c_neg = 0, c_zero = 0, c_pos = 0, c_2x2 = 0, c_del = 0;
+    double minpiv = DBL_MAX;
+    int e = 0, qe = q;
+    while (e < qe) {
+        const int k = e;
+        // column k: FS candidates (k, qe) -> (gC, r); all active rows (k, f) -> gR
+        MaxIdx mC{-1.0, INT_MAX};
+        double mR = 0.0;
+        for (int i = k + 1 + tid; i < f; i += kRefThreads) {
+            const double x = fabs(F[i + (size_t)k * ld]);
+            if (i < qe) mC = better(mC, MaxIdx{x, i});
+            mR = fmax(mR, x);
+        }
+        mC = block_max_idx<kRefThreads>(mC, s_mi);
+        const double gR = block_max<kRefThreads>(mR, s_red);
+        double gC = mC.v > 0.0 ? mC.v : 0.0;
+        const int r = mC.v >= 0.0 ? mC.i : k;
+        const double akk = fabs(F[k + (size_t)k * ld]);
+        if (akk == 0.0 && gR == 0.0) {          // zero column: exact zero pivot
+            c_zero++;
+            minpiv = 0.0;
+            e++;
+            continue;
+        }
+        int kind = 1, j = k;
+        double rho = 0.0;
+        if (akk < kAlpha * gC) {
+            double m = 0.0;
+            for (int i = k + tid; i < qe; i += kRefThreads)
+                if (i != r) m = fmax(m, fabs(symget(F, ld, i, r)));
+            rho = block_max<kRefThreads>(m, s_red);
+            if (akk * rho >= kAlpha * gC * gC) { kind = 1; j = k; }
+            else if (fabs(F[r + (size_t)r * ld]) >= kAlpha * rho) { kind = 1; j = r; }
+            else { kind = 2; j = r; }
+        }
+        if (!root) {
+            bool ok;
+            if (kind == 1) {
+                double cm;
+                if (j == k) cm = gR;
+                else {
+                    double m = 0.0;
+                    for (int i = k + tid; i < f; i += kRefThreads)
+                        if (i != j) m = fmax(m, fabs(symget(F, ld, i, j)));
+                    cm = block_max<kRefThreads>(m, s_red);
+                }
+                ok = fabs(F[j + (size_t)j * ld]) >= u * cm;
+            } else {
+                double m1 = 0.0, m2 = 0.0;
+                for (int i = k + tid; i < f; i += kRefThreads) {
+                    if (i != k && i != r) {
+                        m1 = fmax(m1, fabs(F[i + (size_t)k * ld]));
+                        m2 = fmax(m2, fabs(symget(F, ld, i, r)));
+                    }
+                }
+                const double gk = block_max<kRefThreads>(m1, s_red);
+                const double gr = block_max<kRefThreads>(m2, s_red);
+                const double a11 = F[k + (size_t)k * ld], a21 = F[r + (size_t)k * ld], a22 = F[r + (size_t)r * ld];
+                const double det = a11 * a22 - a21 * a21;
+                if (det == 0.0) ok = false;
+                else {
+                    const double ad = fabs(det);
+                    const double t1 = (fabs(a22) * gk + fabs(a21) * gr) / ad;
+                    const double t2 = (fabs(a21) * gk + fabs(a11) * gr) / ad;
+                    ok = t1 <= 1.0 / u && t2 <= 1.0 / u;
+                }
+            }
+            if (!ok) {                            // delay column k to the parent
+                sym_swap(F, ld, f, k, qe - 1);
+                qe--;
+                c_del++;
+                continue;
+            }
+        }
+        if (kind == 1) {
+            sym_swap(F, ld, f, k, j);
+            const double d = F[k + (size_t)k * ld];
+            const double dinv = 1.0 / d;
+            for (int jj = k + 1 + warp; jj < f; jj += nw) {
+                const double wj = F[jj + (size_t)k * ld] * dinv;
+                double* colj = F + (size_t)jj * ld;
+                const double* colk = F + (size_t)k * ld;
+                for (int i = jj + lane; i < f; i += 32) colj[i] = fma(-colk[i], wj, colj[i]);
+            }
+            __syncthreads();
+            for (int i = k + 1 + tid; i < f; i += kRefThreads) F[i + (size_t)k * ld] *= dinv;
+            __syncthreads();
+            if (d < 0.0) c_neg++; else if (d > 0.0) c_pos++; else c_zero++;
+            minpiv = fmin(minpiv, fabs(d));
+            e += 1;
+        } else {
+            sym_swap(F, ld, f, k + 1, r);
+            const double d11 = F[k + (size_t)k * ld], d21 = F[k + 1 + (size_t)k * ld], d22 = F[k + 1 + (size_t)(k + 1) * ld];
+            const double det = d11 * d22 - d21 * d21;
+            const double i11 = d22 / det, i21 = -d21 / det, i22 = d11 / det;
+            const double* col1 = F + (size_t)k * ld;
+            const double* col2 = F + (size_t)(k + 1) * ld;
+            for (int jj = k + 2 + warp; jj < f; jj += nw) {
+                const double w1 = col1[jj], w2 = col2[jj];
+                const double l1 = w1 * i11 + w2 * i21, l2 = w1 * i21 + w2 * i22;
+                double* colj = F + (size_t)jj * ld;
+                for (int i = jj + lane; i < f; i += 32) colj[i] = colj[i] - col1[i] * l1 - col2[i] * l2;
+            }
+            __syncthreads();
+            for (int i = k + 2 + tid; i < f; i += kRefThreads) {
+                const double w1 = F[i + (size_t)k * ld], w2 = F[i + (size_t)(k + 1) * ld];
+                F[i + (size_t)k * ld] = w1 * i11 + w2 * i21;
+                F[i + (size_t)(k + 1) * ld] = w1 * i21 + w2 * i22;
+            }
+            __syncthreads();
+            // a5: sign(det) in the scaled form (d11/d21)(d22/d21) - 1
+            const double t = (d11 / d21) * (d22 / d21) - 1.0;
+            if (t < 0.0) { c_neg++; c_pos++; }
+            else if (t > 0.0) { if (d11 < 0.0) c_neg += 2; else c_pos += 2; }
+            else { c_zero++; if (d11 + d22 < 0.0) c_neg++; else c_pos++; }
+            const double tr = 0.5 * (d11 + d22);
+            const double disc = sqrt(0.25 * (d11 - d22) * (d11 - d22) + d21 * d21);
+            const double big = fabs(tr) + disc;
+            minpiv = fmin(minpiv, big > 0.0 ? fabs(det) / big : 0.0);
+            c_2x2++;
+            e += 2;
+        }
+    }
+    if (tid == 0) {
+        nd_out[s] = q - e;
+        if (c_neg) atomicAdd(&st->n_neg, c_neg);
+        if (c_zero) atomicAdd(&st->n_zero, c_zero);
+        if (c_pos) atomicAdd(&st->n_pos, c_pos);
+        if (c_2x2) atomicAdd(&st->n_2x2, c_2x2);
+        if (c_del) atomicAdd(&st->n_delayed, c_del);
+        if (minpiv < DBL_MAX) atomic_min_pos_double(&st->minpiv_bits, minpiv);
+    }
+}
+
+__global__ void k_gather(const double* __restrict__ src, const int64_t* __restrict__ idx,
+                         double* __restrict__ dst, int64_t n) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = src[idx[k]];
+}
+
+__global__ void k_reset_stats(ShiftStat* st, int batch) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < batch) {
+        ShiftStat z;
+        z.n_neg = z.n_zero = z.n_pos = z.n_2x2 = z.n_delayed = 0;
+        z.minpiv_bits = (unsigned long long)__double_as_longlong(DBL_MAX);
+        z.smax_bits = 0;
+        z.flags = 0;
+        z.need_slack = 0;
+        st[i] = z;
+    }
+}
+
+}  // namespace
+
+void launch_assemble(const DevPlan& P, int lvl_begin, int nfronts, int batch, cudaStream_t st) {
+    k_assemble<<<dim3(nfronts, batch), kAsmThreads, 0, st>>>(P, lvl_begin);
+}
+
+void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    k_factor_ref<<<dim3(nfronts, batch), kRefThreads, 0, st>>>(P, fronts);
+}
+
+void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st) {
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    if (blocks < 1) blocks = 1;
+    k_gather<<<blocks, 256, 0, st>>>(src, idx, dst, n);
+}
+
+void launch_reset_stats(ShiftStat* st, int batch, cudaStream_t s) {
+    k_reset_stats<<<(batch + 127) / 128, 128, 0, s>>>(st, batch);
+}
+
+}  // namespace kep

@@ -1,0 +1,235 @@
+"""Thin ctypes binding of libkep.so (include/kep.h) — argument marshalling only.
+
+Every step of the numeric path runs in the CUDA kernels behind the C ABI;
+this module never computes anything itself and has no CPU fallback: if the
+shared library is missing it raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libkep.so")
+
+KEP_OK, KEP_EINVAL, KEP_EPATTERN, KEP_ESINGULAR, KEP_ENOTSPD, KEP_ENOMEM, KEP_ECUDA = range(7)
+KEP_ENODEVICE = 10
+ORDER = {"auto": 0, "metis": 1, "natural": 2, "user": 3}
+
+
+class KepError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_status_name(status)}: {msg}")
+        self.status = status
+
+
+class _Opts(C.Structure):
+    _fields_ = [("ordering", C.c_int), ("user_perm", C.POINTER(C.c_int64)), ("amalgamate", C.c_int32),
+                ("nrelax", C.c_int32), ("relax_frac", C.c_double), ("pivot_u", C.c_double),
+                ("tau_sing", C.c_double), ("delay_slack", C.c_int32), ("max_batch", C.c_int32),
+                ("device", C.c_int32), ("stream", C.c_void_p), ("kernel_variant", C.c_int32),
+                ("profile", C.c_int32)]
+
+
+class _Profile(C.Structure):
+    _fields_ = [("ms", C.c_double * 4), ("launches", C.c_int64 * 4), ("schur_flops", C.c_double),
+                ("factor_flops", C.c_double), ("shifts", C.c_int64), ("other_launches", C.c_int64)]
+
+
+KERNEL_CLASSES = ("assemble", "panel", "ref", "schur")
+
+
+class _Info(C.Structure):
+    _fields_ = [("n_neg", C.c_int64), ("n_zero", C.c_int64), ("n_pos", C.c_int64), ("n_2x2", C.c_int64),
+                ("n_delayed", C.c_int64), ("min_abs_pivot", C.c_double), ("max_abs_entry", C.c_double)]
+
+
+class _Analysis(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nnz_lower", C.c_int64), ("n_supervariables", C.c_int64),
+                ("n_fronts", C.c_int64), ("n_levels", C.c_int64), ("max_front", C.c_int64),
+                ("max_level_width", C.c_int64), ("nzf", C.c_int64), ("nzf_exec", C.c_int64),
+                ("flops", C.c_double), ("flops_exec", C.c_double), ("flops_schur", C.c_double),
+                ("sum_cb", C.c_int64), ("arena_bytes", C.c_int64), ("delay_slack", C.c_int32),
+                ("batch", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libkep.so (raises if it has not been built: no silent fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing — run __graft_entry__.build() "
+                              "(python -m paper_1710_05134_b200.build)")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        L.kep_default_opts.argtypes = [P(_Opts)]
+        L.kep_analyze.argtypes = [C.c_int64, P(C.c_int64), P(C.c_int32), P(_Opts), P(C.c_void_p)]
+        L.kep_set_values.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double)]
+        L.kep_set_values_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.kep_inertia.argtypes = [C.c_void_p, C.c_double, P(C.c_int64), P(_Info)]
+        L.kep_inertia_many.argtypes = [C.c_void_p, C.c_int32, P(C.c_double), P(C.c_int64), P(C.c_int), P(_Info)]
+        L.kep_get_analysis.argtypes = [C.c_void_p, P(_Analysis)]
+        L.kep_get_perm.argtypes = [C.c_void_p, P(C.c_int64)]
+        L.kep_get_fronts.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
+        L.kep_destroy.argtypes = [C.c_void_p]
+        L.kep_get_profile.argtypes = [C.c_void_p, P(_Profile)]
+        L.kep_reset_profile.argtypes = [C.c_void_p]
+        L.kep_status_string.argtypes = [C.c_int]
+        L.kep_status_string.restype = C.c_char_p
+        L.kep_last_error.argtypes = [C.c_void_p]
+        L.kep_last_error.restype = C.c_char_p
+        L.kep_version.restype = C.c_char_p
+        for f in ("kep_analyze", "kep_set_values", "kep_set_values_dev", "kep_inertia", "kep_inertia_many",
+                  "kep_get_analysis", "kep_get_perm", "kep_get_fronts", "kep_get_profile", "kep_reset_profile"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _status_name(s: int) -> str:
+    try:
+        return lib().kep_status_string(s).decode()
+    except Exception:
+        return str(s)
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+@dataclass
+class InertiaInfo:
+    n_neg: int
+    n_zero: int
+    n_pos: int
+    n_2x2: int
+    n_delayed: int
+    min_abs_pivot: float
+    max_abs_entry: float
+
+
+class Kep:
+    """One analysed pattern on one device (kep_ctx)."""
+
+    def __init__(self, n, colptr, rowidx, ordering="auto", user_perm=None, amalgamate=True, nrelax=16,
+                 relax_frac=0.05, pivot_u=0.01, tau_sing=1e-14, delay_slack=16, max_batch=16, device=-1,
+                 stream=None, kernel_variant=0, profile=False):
+        L = lib()
+        o = _Opts()
+        L.kep_default_opts(C.byref(o))
+        o.ordering = ORDER[ordering]
+        self._perm_keep = None
+        if user_perm is not None:
+            self._perm_keep = np.ascontiguousarray(user_perm, dtype=np.int64)
+            o.user_perm = _ptr(self._perm_keep, C.c_int64)
+            o.ordering = ORDER["user"]
+        o.amalgamate = int(bool(amalgamate))
+        o.nrelax = int(nrelax)
+        o.relax_frac = float(relax_frac)
+        o.pivot_u = float(pivot_u)
+        o.tau_sing = float(tau_sing)
+        o.delay_slack = int(delay_slack)
+        o.max_batch = int(max_batch)
+        o.device = int(device)
+        o.stream = stream
+        o.kernel_variant = int(kernel_variant)
+        o.profile = int(bool(profile))
+        self.n = int(n)
+        cp = np.ascontiguousarray(colptr, dtype=np.int64)
+        ri = np.ascontiguousarray(rowidx, dtype=np.int32)
+        self.nnz = int(cp[-1])
+        h = C.c_void_p()
+        st = L.kep_analyze(self.n, _ptr(cp, C.c_int64), _ptr(ri, C.c_int32), C.byref(o), C.byref(h))
+        if st != KEP_OK:
+            raise KepError(st, L.kep_last_error(None).decode())
+        self._h = h
+
+    @classmethod
+    def from_pencil(cls, p, **kw):
+        k = cls(p.n, p.colptr, p.rowidx, **kw)
+        return k
+
+    def _check(self, st):
+        if st != KEP_OK:
+            raise KepError(st, lib().kep_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().kep_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_values(self, a, b):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if a.shape != (self.nnz,) or b.shape != (self.nnz,):
+            raise KepError(KEP_EPATTERN, "values do not match the analysed pattern")
+        self._check(lib().kep_set_values(self._h, _ptr(a, C.c_double), _ptr(b, C.c_double)))
+
+    def set_values_dev(self, a_ptr: int, b_ptr: int):
+        self._check(lib().kep_set_values_dev(self._h, C.c_void_p(a_ptr), C.c_void_p(b_ptr)))
+
+    def inertia(self, sigma: float):
+        """Returns (status, nu, InertiaInfo); status KEP_OK or KEP_ESINGULAR."""
+        nu = C.c_int64(-1)
+        info = _Info()
+        st = lib().kep_inertia(self._h, float(sigma), C.byref(nu), C.byref(info))
+        if st not in (KEP_OK, KEP_ESINGULAR):
+            self._check(st)
+        return st, (int(nu.value) if st == KEP_OK else None), InertiaInfo(*[getattr(info, f) for f, _ in _Info._fields_])
+
+    def inertia_many(self, sigmas, with_info=False):
+        s = np.ascontiguousarray(sigmas, dtype=np.float64)
+        m = s.shape[0]
+        nus = np.full(m, -1, dtype=np.int64)
+        per = np.zeros(m, dtype=np.int32)
+        infos = (_Info * max(m, 1))()
+        self._check(lib().kep_inertia_many(self._h, m, _ptr(s, C.c_double), _ptr(nus, C.c_int64),
+                                           _ptr(per, C.c_int), infos if with_info else None))
+        if with_info:
+            return nus, per, [InertiaInfo(*[getattr(infos[i], f) for f, _ in _Info._fields_]) for i in range(m)]
+        return nus, per
+
+    def analysis(self) -> dict:
+        a = _Analysis()
+        self._check(lib().kep_get_analysis(self._h, C.byref(a)))
+        return {f: getattr(a, f) for f, _ in _Analysis._fields_}
+
+    def profile(self) -> dict:
+        pr = _Profile()
+        self._check(lib().kep_get_profile(self._h, C.byref(pr)))
+        return dict(ms={n: pr.ms[i] for i, n in enumerate(KERNEL_CLASSES)},
+                    launches={n: pr.launches[i] for i, n in enumerate(KERNEL_CLASSES)},
+                    schur_flops=pr.schur_flops, factor_flops=pr.factor_flops, shifts=pr.shifts,
+                    other_launches=pr.other_launches)
+
+    def reset_profile(self):
+        self._check(lib().kep_reset_profile(self._h))
+
+    def perm(self) -> np.ndarray:
+        p = np.empty(self.n, dtype=np.int64)
+        self._check(lib().kep_get_perm(self._h, _ptr(p, C.c_int64)))
+        return p
+
+    def fronts(self):
+        nf = self.analysis()["n_fronts"]
+        first = np.empty(nf + 1, dtype=np.int64)
+        parent = np.empty(nf, dtype=np.int64)
+        order = np.empty(nf, dtype=np.int64)
+        self._check(lib().kep_get_fronts(self._h, _ptr(first, C.c_int64), _ptr(parent, C.c_int64), _ptr(order, C.c_int64)))
+        return first, parent, order
+
+
+def version() -> str:
+    return lib().kep_version().decode()

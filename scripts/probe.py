@@ -1,0 +1,26 @@
+"""Quick timing probe of kep_inertia_many on a few configs (development aid)."""
+import sys, time, json
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import kepgen
+from paper_1710_05134_b200 import Kep
+
+def run(p, nshift, variant=0, batch=16):
+    t = time.time(); lo, hi = kepgen.spectral_bounds(p); tb = time.time() - t
+    sig = kepgen.uniform_shifts(lo, hi, nshift)
+    t = time.time(); k = Kep.from_pencil(p, max_batch=batch, kernel_variant=variant); ta = time.time() - t
+    k.set_values(p.a, p.b)
+    nus, st = k.inertia_many(sig[:2])       # warm
+    torch.cuda.synchronize()
+    t = time.time(); nus, st = k.inertia_many(sig); dt = time.time() - t
+    a = k.analysis()
+    print(json.dumps(dict(name=p.name, n=p.n, analyze_s=ta, bounds_s=tb, shifts=nshift, s_per_shift=dt / nshift,
+                          shifts_per_s=nshift / dt, gflops=a["flops"] * nshift / dt / 1e9, nus=nus.tolist()[:8],
+                          st=st.tolist()[:8], analysis=a)), flush=True)
+
+which = sys.argv[1:] or ["c1", "c2"]
+for w in which:
+    if w == "c1": run(kepgen.config(1), 32)
+    if w == "c2": run(kepgen.config(2), 16)
+    if w == "c4s": run(kepgen.tb_pencil(shape=(10, 10, 400), o=4, periodic=(False, False, True), seed=4), 16)

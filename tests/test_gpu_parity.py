@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+nu_sigma is an integer: the bar is bit-exact equality on every shift whose
+gap to the spectrum is certified (readings R4/R5).  Inputs are the
+seeded kepgen pencils; expected values come only from ``oracle/``.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import kepgen
+import oracle
+from paper_1710_05134_b200 import Kep
+from paper_1710_05134_b200.kep import KEP_ESINGULAR, KEP_OK
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _certified(w, sig, rel=1e-6):
+    scale = max(abs(w[0]), abs(w[-1]))
+    gaps = np.min(np.abs(sig[:, None] - w[None, :]), axis=1) / scale
+    return gaps >= rel
+
+
+def _pencil_from_dense(A, B, tol=0.0):
+    n = A.shape[0]
+    mask = (np.abs(np.tril(A)) > tol) | (np.abs(np.tril(B)) > tol)
+    mask |= np.eye(n, dtype=bool)
+    cols, rows = [], []
+    colptr = [0]
+    for j in range(n):
+        r = np.nonzero(mask[j:, j])[0] + j
+        rows.append(r)
+        colptr.append(colptr[-1] + len(r))
+    rowidx = np.concatenate(rows).astype(np.int32)
+    colidx = np.repeat(np.arange(n), np.diff(colptr))
+    return kepgen.Pencil(n=n, colptr=np.array(colptr, np.int64), rowidx=rowidx,
+                         a=A[rowidx, colidx].copy(), b=B[rowidx, colidx].copy(), o=1)
+
+
+def test_spec_examples_on_gpu():
+    g = json.load(open(os.path.join(GOLD, "spec_examples.json")))
+    for case in g["nu"]:
+        A = np.diag(np.array(case["A_diag"], float))
+        B = np.diag(np.array(case["B_diag"], float))
+        p = _pencil_from_dense(A, B)
+        k = Kep.from_pencil(p)
+        k.set_values(p.a, p.b)
+        st, nu, _ = k.inertia(case["sigma"])
+        assert st == KEP_OK and nu == case["nu"], case["cite"]
+    for case in g["inertia"]:
+        S = np.array(case["S"], float)
+        p = _pencil_from_dense(S, np.zeros_like(S), tol=-1)     # dense pattern
+        k = Kep.from_pencil(p)
+        k.set_values(p.a, p.b)
+        st, nu, info = k.inertia(0.0)
+        assert st == KEP_OK
+        assert (info.n_neg, info.n_zero, info.n_pos, info.n_2x2) == (case["neg"], case["zero"], case["pos"], case["n2x2"]), case["cite"]
+
+
+def test_singular_shift_reported():
+    A = np.diag(np.arange(1.0, 11.0))
+    p = _pencil_from_dense(A, np.eye(10))
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    st, nu, info = k.inertia(4.0)       # sigma equals lambda_4: exact zero pivot
+    assert st == KEP_ESINGULAR and nu is None and info.n_zero >= 1
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("u,ordering", [(0.01, "auto"), (0.5, "auto"), (0.01, "natural")])
+def test_c1_all_shifts(u, ordering, variant):
+    p = kepgen.config(1)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    sig = kepgen.uniform_shifts(w[0], w[-1], 32)
+    assert np.all(_certified(w, sig))
+    ref = oracle.nu_eig(A, B, sig, eigvals=w)
+    k = Kep.from_pencil(p, pivot_u=u, ordering=ordering, kernel_variant=variant)
+    k.set_values(p.a, p.b)
+    nus, per, infos = k.inertia_many(sig, with_info=True)
+    assert np.all(per == KEP_OK)
+    assert np.array_equal(nus, ref)
+    for s, i in zip(sig, infos):
+        assert i.n_neg + i.n_zero + i.n_pos == p.n
+    if u == 0.5:
+        assert sum(i.n_delayed for i in infos) > 0       # delayed pivots exercised
+    # single-shift entry point agrees with the batched one
+    st, nu, _ = k.inertia(sig[7])
+    assert st == KEP_OK and nu == ref[7]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("n,seed", [(40, 0), (90, 1)])
+def test_random_dense_pencils(n, seed, variant):
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, n))
+    A = M + M.T
+    np.fill_diagonal(A, 0.0)                 # forces 2x2 pivots
+    R = rng.standard_normal((n, n))
+    B = R.T @ R + n * np.eye(n)
+    p = _pencil_from_dense(A, B, tol=-1)
+    w = oracle.eigvals_pencil(A, B)
+    sig = rng.uniform(w[0] - 0.1, w[-1] + 0.1, 24)
+    sig = sig[_certified(w, sig)]
+    k = Kep.from_pencil(p, kernel_variant=variant)
+    k.set_values(p.a, p.b)
+    nus, per, infos = k.inertia_many(sig, with_info=True)
+    assert np.all(per == KEP_OK)
+    assert np.array_equal(nus, oracle.nu_eig(A, B, sig, eigvals=w))
+    assert sum(i.n_2x2 for i in infos) > 0
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("shape,o,per,uA,u", [((6, 6, 8), 4, (False, False, False), 0.0, 0.01),
+                                              ((5, 4, 12), 2, (False, False, True), 0.08, 0.01),
+                                              ((6, 6, 8), 4, (False, False, False), 0.0, 0.5)])
+def test_twins_closed_form(shape, o, per, uA, u, variant):
+    q = kepgen.twin_pencil(shape, o, periodic=per, uA=uA, uB=0.01, seed=103)
+    w = oracle.twin_eigenvalues(q.meta["twin"])
+    sig = kepgen.uniform_shifts(w[0], w[-1], 24)
+    sig = sig[_certified(w, sig)]
+    k = Kep.from_pencil(q, pivot_u=u, kernel_variant=variant)
+    k.set_values(q.a, q.b)
+    nus, st = k.inertia_many(sig)
+    assert np.all(st == KEP_OK)
+    assert np.array_equal(nus, oracle.nu_twin(q.meta["twin"], sig, w))
+
+
+def test_metamorphic_on_gpu():
+    p = kepgen.tb_pencil(shape=(4, 4, 6), o=3, seed=31)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    sig = kepgen.uniform_shifts(w[0], w[-1], 12)
+    sig = sig[_certified(w, sig)]
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    base, _ = k.inertia_many(sig)
+    assert np.all(np.diff(base) >= 0)                              # monotone in sigma
+    tau = 0.41
+    k.set_values(p.a + tau * p.b, p.b)
+    shifted, _ = k.inertia_many(sig + tau)
+    k.set_values(-p.a, p.b)
+    neg, _ = k.inertia_many(-sig)
+    k.set_values(3.0 * p.a, 3.0 * p.b)
+    scl, _ = k.inertia_many(sig)
+    assert np.array_equal(shifted, base) and np.array_equal(neg, p.n - base) and np.array_equal(scl, base)
+
+
+def test_c2_against_sparse_oracle():
+    p = kepgen.config(2)
+    lo, hi = kepgen.spectral_bounds(p)
+    sig = kepgen.uniform_shifts(lo, hi, 6)
+    so = oracle.SparseOracle(p)
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    nus, st = k.inertia_many(sig)
+    assert np.all(st == KEP_OK)
+    for s, v in zip(sig, nus):
+        # certify: the oracle count is constant on [s - d, s + d]
+        d = 1e-6 * max(abs(lo), abs(hi))
+        r = so.inertia(s)
+        if so.inertia(s - d).n_neg == so.inertia(s + d).n_neg == r.n_neg:
+            assert v == r.n_neg
