@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cfloat>
 #include <cstring>
 #include <new>
@@ -292,6 +294,9 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas) {
         bool over = false;
         for (int i = 0; i < m; ++i)
             if (c->h_stats[i].flags & kep::FLAG_OVERFLOW) { over = true; need = std::max(need, c->h_stats[i].need_slack); }
+        if (getenv("KEP_DEBUG"))
+            fprintf(stderr, "[kep] batch m=%d attempt=%d overflow=%d need=%d slack=%d\n", m, attempt, (int)over, need,
+                    c->sym.slack);
         if (!over) return KEP_OK;
         int slack = std::max(2 * c->sym.slack, need + 8);
         kep_status r = replan(c, slack);

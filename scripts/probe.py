@@ -9,15 +9,17 @@ from paper_1710_05134_b200 import Kep
 def run(p, nshift, variant=0, batch=16):
     t = time.time(); lo, hi = kepgen.spectral_bounds(p); tb = time.time() - t
     sig = kepgen.uniform_shifts(lo, hi, nshift)
-    t = time.time(); k = Kep.from_pencil(p, max_batch=batch, kernel_variant=variant); ta = time.time() - t
+    t = time.time(); k = Kep.from_pencil(p, max_batch=batch, kernel_variant=variant, profile=True); ta = time.time() - t
     k.set_values(p.a, p.b)
     nus, st = k.inertia_many(sig[:2])       # warm
     torch.cuda.synchronize()
+    k.reset_profile()
     t = time.time(); nus, st = k.inertia_many(sig); dt = time.time() - t
+    prof = k.profile()
     a = k.analysis()
     print(json.dumps(dict(name=p.name, n=p.n, analyze_s=ta, bounds_s=tb, shifts=nshift, s_per_shift=dt / nshift,
                           shifts_per_s=nshift / dt, gflops=a["flops"] * nshift / dt / 1e9, nus=nus.tolist()[:8],
-                          st=st.tolist()[:8], analysis=a)), flush=True)
+                          st=st.tolist()[:8], sigma=sig.tolist()[:8], profile=prof, analysis=a)), flush=True)
 
 which = sys.argv[1:] or ["c1", "c2"]
 for w in which:
