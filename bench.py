@@ -342,7 +342,7 @@ def main():
 
     if rank == 0:
         ms = prof["ms"]
-        dom = max(("panel", "schur", "ref", "assemble"), key=lambda x: ms[x])
+        dom = max(ms, key=lambda x: ms[x])
         sch_t = ms["schur"] / 1e3
         roof = {"bound": "tensor", "kernel": "k_schur (a4, DMMA f64)",
                 "achieved": (prof["schur_flops"] / sch_t / 1e12) if sch_t > 0 else None,

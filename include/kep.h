@@ -88,10 +88,14 @@ typedef struct {
 
 /* Kernel classes for kep_profile (rows of SURVEY.md §8(a)). */
 enum { KEP_K_ASSEMBLE = 0,   /* a1 + a2: assembly + extend-add */
-       KEP_K_PANEL = 1,      /* a3 + a5: blocked Bunch-Kaufman panel (FS columns) */
-       KEP_K_REF = 2,        /* a3 + a4 + a5: reference unblocked front factorisation */
+       KEP_K_PANEL = 1,      /* a3: blocked Bunch-Kaufman on the FS x FS block (k_fs) */
+       KEP_K_REF = 2,        /* a3 + a4 + a5: reference unblocked front factorisation (variant 1, fronts
+                                too large for the fast path, fronts that failed the full-column test) */
        KEP_K_SCHUR = 3,      /* a4: DMMA contribution-block update */
-       KEP_K_NCLASS = 4 };
+       KEP_K_L21 = 4,        /* a3: CB rows of the FS columns, W21 = A21 P^T L11^-T (k_l21) */
+       KEP_K_CHECK = 5,      /* a3 + a5: full-column threshold tests, inertia, D^-1 coefficients */
+       KEP_K_FSU = 6,        /* a3: FS x FS trailing update after each pivot block (k_fsu) */
+       KEP_K_NCLASS = 7 };
 
 typedef struct {
     double ms[KEP_K_NCLASS];          /* summed CUDA-event time per class (profile = 1 only) */
@@ -109,6 +113,8 @@ typedef struct {
     int64_t n_delayed;              /* columns delayed to a parent front (sum over fronts) */
     double min_abs_pivot;           /* min over blocks of the smallest |eigenvalue| */
     double max_abs_entry;           /* max |a_ij - sigma b_ij| */
+    int64_t n_redo;                 /* fronts whose full-column threshold test failed on the fast
+                                       path and were refactorised by the unblocked kernel */
 } kep_inertia_info;
 
 typedef struct {

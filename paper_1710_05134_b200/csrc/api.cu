@@ -48,8 +48,19 @@ struct kep_ctx {
     // per-level launch lists: fast (panel + Schur) and reference fronts
     int32_t* d_lists = nullptr;                 // [fast fronts of all levels | ref fronts of all levels]
     int4* d_items = nullptr;                    // Schur tiles (front, I, J, 0)
-    std::vector<int64_t> fast_off, fast_cnt, ref_off, ref_cnt, item_off, item_cnt;
-    int max_fast_cap = 0;
+    int4* d_litems = nullptr;                   // k_l21 row tiles (front, I, 0, 0)
+    std::vector<int64_t> fast_off, fast_cnt, ref_off, ref_cnt, item_off, item_cnt, litem_off, litem_cnt;
+    // fast-path pivot records: per-front offsets (entries), per shift stride (doubles)
+    int64_t* d_aux_off = nullptr;
+    int64_t aux_stride = 0;
+    double* d_aux = nullptr;
+    int32_t* d_flag = nullptr;
+    int32_t* d_forced = nullptr;
+    int32_t* d_fstate = nullptr;
+    int32_t* d_pending = nullptr;                // fronts flagged for a fast-path rerun (per level)
+    int4* d_uitems = nullptr;                   // k_fsu tiles (front, I, J, 0)
+    std::vector<int64_t> uitem_off, uitem_cnt;
+    std::vector<int> level_qmax;                // per level: max p + slack over its fast fronts
     std::vector<double> item_flops;             // per level: algorithmic a4 flops of its fast fronts
     // profiling
     kep_profile prof;
@@ -60,6 +71,7 @@ struct kep_ctx {
 namespace {
 
 thread_local std::string g_err;
+constexpr int kReruns = 2;      // fast-path reruns per level before the unblocked fallback
 
 kep_status fail(kep_ctx* c, kep_status s, const std::string& msg) {
     if (c) c->err = msg;
@@ -91,6 +103,11 @@ void free_batch(kep_ctx* c) {
     cudaFree(c->d_doff); c->d_doff = nullptr;
     cudaFree(c->d_stats); c->d_stats = nullptr;
     cudaFree(c->d_sigma); c->d_sigma = nullptr;
+    cudaFree(c->d_aux); c->d_aux = nullptr;
+    cudaFree(c->d_flag); c->d_flag = nullptr;
+    cudaFree(c->d_forced); c->d_forced = nullptr;
+    cudaFree(c->d_fstate); c->d_fstate = nullptr;
+    cudaFree(c->d_pending); c->d_pending = nullptr;
 }
 
 // (Re)allocate the per-batch state for the current memory plan.
@@ -98,7 +115,7 @@ kep_status alloc_batch(kep_ctx* c) {
     free_batch(c);
     size_t freeb = 0, totalb = 0;
     KEP_CUDA(c, cudaMemGetInfo(&freeb, &totalb));
-    const size_t per_shift = (size_t)c->sym.arena_doubles * sizeof(double);
+    const size_t per_shift = ((size_t)c->sym.arena_doubles + (size_t)c->aux_stride) * sizeof(double);
     int cap = std::max(1, c->opts.max_batch);
     const size_t budget = (size_t)(0.85 * (double)freeb);
     while (cap > 1 && per_shift * (size_t)cap > budget) cap--;
@@ -112,6 +129,12 @@ kep_status alloc_batch(kep_ctx* c) {
     KEP_CUDA(c, cudaMalloc(&c->d_doff, nfb));
     KEP_CUDA(c, cudaMalloc(&c->d_stats, sizeof(ShiftStat) * cap));
     KEP_CUDA(c, cudaMalloc(&c->d_sigma, sizeof(double) * cap));
+    KEP_CUDA(c, cudaMalloc(&c->d_aux, sizeof(double) * std::max<int64_t>(c->aux_stride, 1) * cap));
+    KEP_CUDA(c, cudaMalloc(&c->d_flag, nfb));
+    KEP_CUDA(c, cudaMemset(c->d_flag, 0, nfb));
+    KEP_CUDA(c, cudaMalloc(&c->d_forced, nfb * (kep::FMAX + 1)));
+    KEP_CUDA(c, cudaMalloc(&c->d_fstate, nfb * kep::FSTATE_W));
+    KEP_CUDA(c, cudaMalloc(&c->d_pending, sizeof(int32_t)));
     c->h_stats.resize(cap);
     return KEP_OK;
 }
@@ -121,23 +144,30 @@ kep_status alloc_batch(kep_ctx* c) {
 kep_status build_lists(kep_ctx* c) {
     const Symbolic& S = c->sym;
     const int nl = (int)S.level_ptr.size() - 1;
-    const int lim = kep::panel_max_front();
     const bool use_fast = c->opts.kernel_variant == 0;
     std::vector<int32_t> fast, ref;
-    std::vector<int4> items;
+    std::vector<int4> items, litems, uitems;
+    c->litem_off.assign(nl, 0); c->litem_cnt.assign(nl, 0);
+    c->uitem_off.assign(nl, 0); c->uitem_cnt.assign(nl, 0);
     c->fast_off.assign(nl, 0); c->fast_cnt.assign(nl, 0);
     c->ref_off.assign(nl, 0); c->ref_cnt.assign(nl, 0);
     c->item_off.assign(nl, 0); c->item_cnt.assign(nl, 0);
-    c->max_fast_cap = 0;
+    c->level_qmax.assign(nl, 0);
     for (int L = 0; L < nl; ++L) {
         c->fast_off[L] = (int64_t)fast.size();
         c->ref_off[L] = (int64_t)ref.size();
         c->item_off[L] = (int64_t)items.size();
+        c->litem_off[L] = (int64_t)litems.size();
+        c->uitem_off[L] = (int64_t)uitems.size();
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
             const int s = S.level_fronts[k];
-            if (use_fast && S.capacity[s] <= lim) {
+            const int qcap = S.capacity[s] - S.ncb[s];            // p + slack
+            if (use_fast && kep::front_nb_for(qcap) > 0) {
                 fast.push_back(s);
-                c->max_fast_cap = std::max(c->max_fast_cap, (int)S.capacity[s]);
+                c->level_qmax[L] = std::max(c->level_qmax[L], qcap);
+                for (int I = 0; I < (S.ncb[s] + 63) / 64; ++I) litems.push_back(make_int4(s, I, 0, 0));
+                for (int I = 0; I < (qcap + 63) / 64; ++I)
+                    for (int J = 0; J <= I; ++J) uitems.push_back(make_int4(s, I, J, 0));
                 const int nt = (S.ncb[s] + 63) / 64;
                 for (int I = 0; I < nt; ++I)
                     for (int J = 0; J <= I; ++J) items.push_back(make_int4(s, I, J, 0));
@@ -148,6 +178,8 @@ kep_status build_lists(kep_ctx* c) {
         c->fast_cnt[L] = (int64_t)fast.size() - c->fast_off[L];
         c->ref_cnt[L] = (int64_t)ref.size() - c->ref_off[L];
         c->item_cnt[L] = (int64_t)items.size() - c->item_off[L];
+        c->litem_cnt[L] = (int64_t)litems.size() - c->litem_off[L];
+        c->uitem_cnt[L] = (int64_t)uitems.size() - c->uitem_off[L];
     }
     c->item_flops.assign(nl, 0.0);
     for (int L = 0; L < nl; ++L)
@@ -161,6 +193,20 @@ kep_status build_lists(kep_ctx* c) {
     for (int L = 0; L < nl; ++L) c->ref_off[L] += nfast;
     cudaFree(c->d_lists); c->d_lists = nullptr;
     cudaFree(c->d_items); c->d_items = nullptr;
+    cudaFree(c->d_litems); c->d_litems = nullptr;
+    cudaFree(c->d_uitems); c->d_uitems = nullptr;
+    KEP_CUDA(c, upload(&c->d_uitems, uitems));
+    cudaFree(c->d_aux_off); c->d_aux_off = nullptr;
+    KEP_CUDA(c, upload(&c->d_litems, litems));
+    // pivot-record offsets: Q_s = p_s + slack entries per front
+    std::vector<int64_t> aoff(S.nf > 0 ? S.nf : 1, 0);
+    int64_t acc = 0;
+    for (int64_t f2 = 0; f2 < S.nf; ++f2) {
+        aoff[f2] = acc;
+        acc += S.capacity[f2] - S.ncb[f2];
+    }
+    c->aux_stride = std::max<int64_t>(acc, 1) * kep::AUX_W;
+    KEP_CUDA(c, upload(&c->d_aux_off, aoff));
     KEP_CUDA(c, upload(&c->d_lists, lists));
     KEP_CUDA(c, upload(&c->d_items, items));
     return KEP_OK;
@@ -227,6 +273,14 @@ DevPlan make_plan(kep_ctx* c) {
     P.stats = c->d_stats;
     P.sigma = c->d_sigma;
     P.u = c->opts.pivot_u;
+    P.aux = c->d_aux;
+    P.aux_stride = c->aux_stride;
+    P.aux_off = c->d_aux_off;
+    P.flag = c->d_flag;
+    P.forced = c->d_forced;
+    P.fstate = c->d_fstate;
+    P.pending = c->d_pending;
+    P.debug = getenv("KEP_DEBUG") ? 1 : 0;
     return P;
 }
 
@@ -237,6 +291,8 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas) {
         KEP_CUDA(c, cudaMemcpyAsync(c->d_sigma, sigmas, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
         kep::launch_reset_stats(c->d_stats, m, c->stream);
         c->prof.other_launches += 1;
+        if (const char* fill = getenv("KEP_DEBUG_FILL"))       // debug: poison the front arena
+            cudaMemsetAsync(c->d_arena, atoi(fill) & 0xff, c->arena_alloc_doubles * sizeof(double), c->stream);
         DevPlan P = make_plan(c);
         const Symbolic& S = c->sym;
         const int nl = (int)S.level_ptr.size() - 1;
@@ -261,10 +317,46 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas) {
             mark(KEP_K_ASSEMBLE, false);
             c->prof.launches[KEP_K_ASSEMBLE]++;
             if (c->fast_cnt[L]) {
-                mark(KEP_K_PANEL, true);
-                kep::launch_panel(P, c->d_lists + c->fast_off[L], (int)c->fast_cnt[L], m, c->max_fast_cap, c->stream);
-                mark(KEP_K_PANEL, false);
-                c->prof.launches[KEP_K_PANEL]++;
+                const int32_t* fl = c->d_lists + c->fast_off[L];
+                const int nfl2 = (int)c->fast_cnt[L];
+                // pass 0, then kReruns passes over the fronts whose full-column test failed
+                // (each with one more forced delay), then the unblocked kernel for the rest
+                const int iters = kep::fs_iters(c->level_qmax[L]);
+                for (int pass = 0; pass <= kReruns; ++pass) {
+                    if (pass > 0) {                     // any front flagged for a rerun at this level?
+                        int32_t pend = 0;
+                        KEP_CUDA(c, cudaMemcpyAsync(&pend, c->d_pending, sizeof(pend), cudaMemcpyDeviceToHost, c->stream));
+                        KEP_CUDA(c, cudaStreamSynchronize(c->stream));
+                        if (pend == 0) break;
+                    }
+                    KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, sizeof(int32_t), c->stream));
+                    for (int itn = 0; itn < iters; ++itn) {
+                        mark(KEP_K_PANEL, true);
+                        kep::launch_fsp(P, fl, nfl2, m, c->level_qmax[L], itn == 0 ? (pass == 0 ? 0 : 1) : 2, c->stream);
+                        mark(KEP_K_PANEL, false);
+                        c->prof.launches[KEP_K_PANEL]++;
+                        if (c->uitem_cnt[L]) {
+                            mark(KEP_K_FSU, true);
+                            kep::launch_fsu(P, c->d_uitems + c->uitem_off[L], (int)c->uitem_cnt[L], m, c->stream);
+                            mark(KEP_K_FSU, false);
+                            c->prof.launches[KEP_K_FSU]++;
+                        }
+                    }
+                    if (c->litem_cnt[L]) {
+                        mark(KEP_K_L21, true);
+                        kep::launch_l21(P, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, c->stream);
+                        mark(KEP_K_L21, false);
+                        c->prof.launches[KEP_K_L21]++;
+                    }
+                    mark(KEP_K_CHECK, true);
+                    kep::launch_check(P, fl, nfl2, m, c->stream);
+                    mark(KEP_K_CHECK, false);
+                    c->prof.launches[KEP_K_CHECK]++;
+                }
+                mark(KEP_K_REF, true);
+                kep::launch_factor_list(P, fl, nfl2, m, c->stream, true);
+                mark(KEP_K_REF, false);
+                c->prof.launches[KEP_K_REF]++;
             }
             if (c->ref_cnt[L]) {
                 mark(KEP_K_REF, true);
@@ -466,6 +558,7 @@ kep_status kep_inertia_many(kep_ctx* c, int32_t m, const double* sigmas, int64_t
                 I.n_delayed = (int64_t)s.n_delayed;
                 I.min_abs_pivot = minpiv >= DBL_MAX ? 0.0 : minpiv;
                 I.max_abs_entry = smax;
+                I.n_redo = (int64_t)s.n_redo;
             }
         }
         done += got;
@@ -543,7 +636,8 @@ void kep_destroy(kep_ctx* c) {
         free_batch(c);
         void* ptrs[] = {c->d_forder, c->d_npiv, c->d_ncb, c->d_cap, c->d_child_ptr, c->d_child_list,
                         c->d_level_fronts, c->d_arena_off, c->d_asm_ptr, c->d_asm_src, c->d_rmap_ptr,
-                        c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items};
+                        c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
+                        c->d_litems, c->d_aux_off, c->d_uitems};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -7,7 +7,7 @@ namespace kep {
 
 // Per-shift counters (one per shift of a batch); reset before every batch.
 struct ShiftStat {
-    unsigned long long n_neg, n_zero, n_pos, n_2x2, n_delayed;
+    unsigned long long n_neg, n_zero, n_pos, n_2x2, n_delayed, n_redo;
     unsigned long long minpiv_bits;   // min |pivot| as positive-double bits (init +inf)
     unsigned long long smax_bits;     // max |a - sigma b| as positive-double bits (init 0)
     int flags;                        // bit 0: delayed-pivot slack overflow
@@ -42,7 +42,42 @@ struct DevPlan {
     ShiftStat* stats;            // [batch]
     const double* sigma;         // [batch]
     double u;                    // threshold pivoting parameter
+    // fast path (kernels_front.cu): per-front pivot records and redo flags
+    double* aux;                 // [batch][aux_stride]
+    int64_t aux_stride;          // doubles per shift
+    const int64_t* aux_off;      // [nf] record offset (entries; AUX_W doubles each)
+    int32_t* flag;               // [batch][nf] fast-path state of the front, FL_* below
+    int32_t* forced;             // [batch][nf][FMAX+1] count, then S1 steps at which to delay
+    int32_t* fstate;             // [batch][nf][FSTATE_W] k_fsp state: e, qe, step, forced cursor, block start
+    int32_t* pending;            // count of fronts flagged FL_RERUN in the current level
+    int32_t debug;               // KEP_DEBUG set: diagnostic printf in rare paths
 };
+
+// pivot kinds recorded per eliminated position
+constexpr int PK_1X1 = 0, PK_2X2A = 1, PK_2X2B = 2, PK_ZERO = 3;
+constexpr int AUX_W = 8;         // doubles per position: diag backup, d, ds, fa, fb, cm, (kind, perm), (step, -)
+// front states: FL_OK = factorised, FL_REF = hand to the unblocked kernel,
+// FL_RERUN = rerun the fast path with one more forced delay, FL_ACTIVE = in the current fast pass
+constexpr int FL_OK = 0, FL_REF = 1, FL_RERUN = 2, FL_ACTIVE = 3;
+constexpr int FSTATE_W = 8;
+constexpr int FMAX = 6;          // forced delays per front before falling back to the unblocked kernel
+
+struct AuxRec {
+    double *diag, *d, *ds, *fa, *fb;
+    unsigned long long* cm;      // CB column maxima of W21 (positive-double bits)
+    int *kind, *perm, *step;
+};
+
+__device__ __forceinline__ AuxRec aux_rec(const DevPlan& P, int sh, int s, int Q) {
+    double* b = P.aux + (size_t)sh * P.aux_stride + (size_t)P.aux_off[s] * AUX_W;
+    AuxRec A;
+    A.diag = b; A.d = b + Q; A.ds = b + 2 * Q; A.fa = b + 3 * Q; A.fb = b + 4 * Q;
+    A.cm = (unsigned long long*)(b + 5 * Q);
+    A.kind = (int*)(b + 6 * Q);
+    A.perm = A.kind + Q;
+    A.step = (int*)(b + 7 * Q);
+    return A;
+}
 
 __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
     atomicMax(addr, (unsigned long long)__double_as_longlong(v));
@@ -51,12 +86,17 @@ __device__ __forceinline__ void atomic_min_pos_double(unsigned long long* addr, 
     atomicMin(addr, (unsigned long long)__double_as_longlong(v));
 }
 
-// Launchers (kernels.cu)
+// Launchers (kernels.cu, kernels_front.cu, kernels_fast.cu)
 void launch_assemble(const DevPlan& P, int lvl_begin, int nfronts, int batch, cudaStream_t st);
-void launch_panel(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int max_f, cudaStream_t st);
+void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st);
+void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
+int fs_iters(int qmax);               // k_fsp launches that finish every front of a level
+void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
+void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
+int front_nb_for(int qmax);           // block width for a level (0: too large, use the reference kernel)
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
-int panel_max_front();
-void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
+void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,
+                        bool only_flagged = false);
 void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st);
 void launch_reset_stats(ShiftStat* st, int batch, cudaStream_t s);
 

@@ -189,9 +189,10 @@ __device__ void sym_swap(double* F, int ld, int f, int a, int b) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int32_t* __restrict__ fronts) {
+__global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int32_t* __restrict__ fronts, int only_flagged) {
     const int s = fronts[blockIdx.x];
     const int sh = blockIdx.y;
+    if (only_flagged && P.flag[(size_t)sh * P.nf + s] == 0) return;   // fast path kept this front
     ShiftStat* st = P.stats + sh;
     const int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
     int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
                     ok = t1 <= 1.0 / u && t2 <= 1.0 / u;
                 }
             }
+            __syncthreads();                      // every thread has read the pivot entries
             if (!ok) {                            // delay column k to the parent
                 sym_swap(F, ld, f, k, qe - 1);
                 qe--;
@@ -282,6 +284,7 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
                 continue;
             }
         }
+        if (root) __syncthreads();                // (non-root fronts synchronised above)
         if (kind == 1) {
             sym_swap(F, ld, f, k, j);
             const double d = F[k + (size_t)k * ld];
@@ -352,7 +355,7 @@ __global__ void k_reset_stats(ShiftStat* st, int batch) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < batch) {
         ShiftStat z;
-        z.n_neg = z.n_zero = z.n_pos = z.n_2x2 = z.n_delayed = 0;
+        z.n_neg = z.n_zero = z.n_pos = z.n_2x2 = z.n_delayed = z.n_redo = 0;
         z.minpiv_bits = (unsigned long long)__double_as_longlong(DBL_MAX);
         z.smax_bits = 0;
         z.flags = 0;
@@ -367,9 +370,10 @@ void launch_assemble(const DevPlan& P, int lvl_begin, int nfronts, int batch, cu
     k_assemble<<<dim3(nfronts, batch), kAsmThreads, 0, st>>>(P, lvl_begin);
 }
 
-void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,
+                        bool only_flagged) {
     if (nfronts <= 0) return;
-    k_factor_ref<<<dim3(nfronts, batch), kRefThreads, 0, st>>>(P, fronts);
+    k_factor_ref<<<dim3(nfronts, batch), kRefThreads, 0, st>>>(P, fronts, only_flagged ? 1 : 0);
 }
 
 void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st) {

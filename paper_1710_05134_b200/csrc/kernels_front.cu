@@ -1,0 +1,862 @@
+// kernels_front.cu — rows a3 + a5 of SURVEY.md §8 for the fast path: partial
+// LDL^T of the fully-summed (FS) columns of every front of one level with
+// Bunch–Kaufman pivoting, the threshold test and delayed pivots (DESIGN.md
+// reading R1; PAPER.md:86 cites Bunch–Kaufman; Alg. 1' line 3, PAPER.md:419,
+// factorises A - sigma B).
+//
+// Front  F = [A11 A21^T; A21 A22]  (A11: q x q FS block, A21: c x q CB rows).
+// Partial factorisation  P A11 P^T = L11 D11 L11^T,  W21 = A21 P^T L11^-T,
+// L21 = W21 D11^-1,  Schur complement A22 - W21 L21^T (row a4, k_schur).
+//
+// The threshold test of R1 compares a pivot with the maximum of its whole
+// current column, FS rows AND CB rows.  Every such maximum is
+// max(FS part, CB part), and the CB part of the column eliminated at
+// position t is exactly max_i |W21[i, t]|.  So the rule is applied in three
+// kernels per level:
+//
+//  k_fs    one CTA per (front, shift): the FS x FS block only.  Blocks of NB
+//          pivots, raw block columns in shared memory, candidate columns
+//          brought up to date on demand (left-looking inside the block), BK
+//          choice (alpha = (1+sqrt17)/8) among the FS candidates, threshold
+//          test with the FS maxima (a column failing there is delayed — the
+//          full test fails too), rank-nb DMMA update of the FS trailing
+//          block.  The assembled A11 is kept (transposed) in the free upper
+//          triangle so the front can be restored.  Records, per position,
+//          the pivot kind, D, the FS maxima and the permutation.
+//  k_l21   many CTAs per front: 64 CB rows each, the unit-triangular solve
+//          W21 = A21 P^T L11^-T (DMMA for the off-block part), written to
+//          the upper triangle of the CB columns, and the column maxima of
+//          W21 (the CB parts of the tests).
+//  k_check one CTA per front: re-evaluates every test in pivot order with
+//          the full-column maxima.  All pass -> the pivot sequence is the
+//          unblocked rule's; inertia is counted and L21 = W21 D^-1 written.
+//          A failure -> the front is restored to its assembled state and
+//          flagged; k_factor_ref (the unblocked rule itself) redoes it.
+//
+// Storage per front (column-major, ld = f):  L[i,t] at F[i + t*ld] (i > t;
+// 0 at the subdiagonal of a 2x2 block, whose D lives in the aux record),
+// W21[i,t] at F[t + i*ld] for CB rows i.
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+#include <cstdio>
+
+#include "device.cuh"
+
+namespace kep {
+
+namespace {
+
+constexpr double kAlpha = 0.6403882032022076;   // (1 + sqrt(17)) / 8
+constexpr int FT = 256;                         // k_fs / k_check threads
+constexpr int LT = 128;                         // k_l21 threads (4 warps x 16 rows)
+constexpr int LR = 64;                          // k_l21 CB rows per CTA
+constexpr int LB = 32;                          // k_l21 column block
+constexpr int KC = 16;                          // K chunk of the k_l21 GEMM
+constexpr int APAD = LR + 4;                    // = 4 (mod 16): conflict-free f64 fragments
+constexpr int BP = KC + 4;
+
+struct MaxIdx {
+    double v;
+    int i;
+};
+
+__device__ __forceinline__ MaxIdx better(MaxIdx a, MaxIdx b) {
+    if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+    return a;
+}
+
+struct Red {
+    MaxIdx mi[FT / 32];
+    double x[3][FT / 32];
+};
+
+// block-wide (max, argmax) of a and max of b, c, d
+__device__ void block_reduce(MaxIdx& a, double& b, double& c, double& d, Red* R) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        MaxIdx y;
+        y.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+        y.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+        a = better(a, y);
+        b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        c = fmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+        d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) { R->mi[w] = a; R->x[0][w] = b; R->x[1][w] = c; R->x[2][w] = d; }
+    __syncthreads();
+    a = R->mi[0]; b = R->x[0][0]; c = R->x[1][0]; d = R->x[2][0];
+#pragma unroll
+    for (int q = 1; q < FT / 32; ++q) {
+        a = better(a, R->mi[q]);
+        b = fmax(b, R->x[0][q]);
+        c = fmax(c, R->x[1][q]);
+        d = fmax(d, R->x[2][q]);
+    }
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    const int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Symmetric interchange of FS positions a < b in the lower FS x FS block
+// (rows/columns of the active part and L rows of the columns t < a).
+__device__ void sym_swap_fs(double* F, int ld, int q, int a, int b) {
+    if (a == b) return;
+    for (int t = threadIdx.x; t < q; t += FT) {
+        if (t < a) {
+            double* x = F + a + (size_t)t * ld;
+            double* y = F + b + (size_t)t * ld;
+            double v = *x; *x = *y; *y = v;
+        } else if (t == a) {
+            double* x = F + a + (size_t)a * ld;
+            double* y = F + b + (size_t)b * ld;
+            double v = *x; *x = *y; *y = v;
+        } else if (t < b) {
+            double* x = F + t + (size_t)a * ld;
+            double* y = F + b + (size_t)t * ld;
+            double v = *x; *x = *y; *y = v;
+        } else if (t > b) {
+            double* x = F + t + (size_t)a * ld;
+            double* y = F + t + (size_t)b * ld;
+            double v = *x; *x = *y; *y = v;
+        }
+    }
+}
+
+template <int NB>
+struct Smem {
+    double* Ls;            // [NB][RS] block columns by position row (i - kp); raw, then L
+    double* wk;            // [RS] updated column k (FS rows)
+    double* wr;            // [RS] updated column r
+    double* cs;            // [NB] W = Ls[t]*cs + Ls[t+oo]*co  (W = L D)
+    double* co;
+    double* wrow;          // [NB]
+    double* wrowr;         // [NB]
+    double* d1;            // [NB] D diagonal / 2x2 entries, FS maxima of the tests
+    double* d2;
+    double* fa;
+    double* fb;
+    int* oo;               // [NB] 2x2 partner offset (0 / +1 / -1)
+    int* tp;               // [NB] kind per block column
+    int* st;               // [NB] S1 step index per block column
+    int* perm;             // [RS] original FS column at each position
+    Red* red;
+};
+
+template <int NB>
+__device__ Smem<NB> carve(double* base, int RS) {
+    Smem<NB> S;
+    double* p = base;
+    S.Ls = p; p += (size_t)NB * RS;
+    S.wk = p; p += RS;
+    S.wr = p; p += RS;
+    S.cs = p; p += NB;
+    S.co = p; p += NB;
+    S.wrow = p; p += NB;
+    S.wrowr = p; p += NB;
+    S.d1 = p; p += NB;
+    S.d2 = p; p += NB;
+    S.fa = p; p += NB;
+    S.fb = p; p += NB;
+    S.red = (Red*)p; p += (sizeof(Red) + 7) / 8;
+    S.oo = (int*)p; p += (NB + 1) / 2;
+    S.tp = (int*)p; p += (NB + 1) / 2;
+    S.st = (int*)p; p += (NB + 1) / 2;
+    S.perm = (int*)p; p += (RS + 1) / 2;
+    return S;
+}
+
+}  // namespace
+
+size_t fs_smem_bytes(int nb, int RS) {
+    size_t d = (size_t)nb * RS + 2 * (size_t)RS + 8 * nb + (sizeof(Red) + 7) / 8 + 3 * ((nb + 1) / 2) + (RS + 1) / 2;
+    return d * sizeof(double);
+}
+
+namespace {
+
+template <int NB>
+__device__ __forceinline__ double wform(const Smem<NB>& S, int RS, int t, int ii) {
+    // W[position kp+ii, block column t]
+    const double* L = S.Ls + (size_t)t * RS + ii;
+    const int o = S.oo[t];
+    return L[0] * S.cs[t] + (o ? L[(ptrdiff_t)o * RS] * S.co[t] : 0.0);
+}
+
+// After the global interchange of positions a < b: L rows a, b of all block
+// columns (raw ones included), whole raw columns a, b reloaded, rows a, b of
+// the other raw columns reloaded.  kfirst = first raw (not yet pivoted) column.
+template <int NB>
+__device__ void swap_block(const Smem<NB>& S, int RS, const double* F, int ld, int q, int kp, int kfirst, int a, int b,
+                           int* perm) {
+    const int tid = threadIdx.x;
+    __syncthreads();                                   // global interchange complete
+    for (int t = tid; t < NB; t += FT) {
+        double* col = S.Ls + (size_t)t * RS;
+        const double x = col[a - kp];
+        col[a - kp] = col[b - kp];
+        col[b - kp] = x;
+    }
+    if (tid == 0) { const int x = perm[a]; perm[a] = perm[b]; perm[b] = x; }
+    __syncthreads();
+    const int hi = min(kp + NB, q);
+    for (int j = kfirst + tid; j < hi; j += FT) {
+        if (j == a || j == b) continue;
+        double* col = S.Ls + (size_t)(j - kp) * RS;
+        if (a >= j) col[a - kp] = F[a + (size_t)j * ld];
+        if (b >= j) col[b - kp] = F[b + (size_t)j * ld];
+    }
+    const int cols[2] = {a, b};
+    for (int x = 0; x < 2; ++x) {
+        const int j = cols[x];
+        if (j < kfirst || j >= hi) continue;
+        double* col = S.Ls + (size_t)(j - kp) * RS;
+        for (int i = j + tid; i < q; i += FT) col[i - kp] = F[i + (size_t)j * ld];
+    }
+    __syncthreads();
+}
+
+template <int NB>
+__device__ void do_swap(const Smem<NB>& S, int RS, double* F, int ld, int q, int kp, int kfirst, int a, int b, int* perm) {
+    if (a == b) return;
+    sym_swap_fs(F, ld, q, a, b);
+    swap_block<NB>(S, RS, F, ld, q, kp, kfirst, a, b, perm);
+}
+
+template <int NB>
+// One block of at most NB pivots per launch (mode 0: first block of pass 0;
+// mode 1: first block of a rerun pass; mode 2: next block).  The state between
+// launches (e, qe, S1 step, forced-delay cursor, block start) lives in fstate.
+__global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restrict__ fronts, int RS, int mode) {
+    extern __shared__ __align__(16) double dyn[];
+    const Smem<NB> S = carve<NB>(dyn, RS);
+    const int s = fronts[blockIdx.x];
+    const int sh = blockIdx.y;
+    const int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
+    int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
+    const int nd = nd_in[s];
+    int32_t* flag = P.flag + (size_t)sh * P.nf + s;
+    int32_t* forced = P.forced + ((size_t)sh * P.nf + s) * (FMAX + 1);
+    int32_t* fst = P.fstate + ((size_t)sh * P.nf + s) * FSTATE_W;
+    if (mode == 2) {
+        if (*flag != FL_ACTIVE) return;
+        const bool done = fst[0] >= fst[1];
+        __syncthreads();
+        if (threadIdx.x == 0) fst[5] = 0;                // the previous block's update has been applied
+        if (done) return;
+    } else if (mode == 1) {
+        if (*flag != FL_RERUN) return;
+    } else if (threadIdx.x == 0) {
+        forced[0] = 0;
+    }
+    if (nd < 0) {
+        if (threadIdx.x == 0) { nd_out[s] = -1; *flag = FL_OK; }
+        return;
+    }
+    __shared__ int s_forced[FMAX + 1];
+    if (threadIdx.x <= FMAX) s_forced[threadIdx.x] = mode ? forced[threadIdx.x] : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = FL_ACTIVE;
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    (void)f;
+    const bool root = (c == 0);
+    const double u = P.u;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, tg = lane & 3;
+    const int Q = P.cap[s] - c;
+    AuxRec A = aux_rec(P, sh, s, Q);
+
+    int e = 0, qe = q;
+    int step = 0, fnext = 0;                           // S1 actions so far; next forced delay
+    if (mode < 2) {
+        // keep the assembled A11 (strict lower -> upper, diagonal -> aux) for a restore
+        if (!root) {
+            for (int j = warp; j < q; j += FT / 32) {
+                for (int i = j + 1 + lane; i < q; i += 32) F[j + (size_t)i * ld] = F[i + (size_t)j * ld];
+                if (lane == 0) A.diag[j] = F[j + (size_t)j * ld];
+            }
+        }
+        for (int i = tid; i < q; i += FT) { A.perm[i] = i; A.cm[i] = 0ull; }
+    } else {
+        e = fst[0]; qe = fst[1]; step = fst[2]; fnext = fst[3];
+    }
+    __syncthreads();
+    const int kp = e;
+    {
+        {   // raw block columns [kp, kp+NB), rows [j, q)
+            const int npre = min(NB, q - kp), R = q - kp;
+            for (int idx = tid; idx < npre * R; idx += FT) {
+                const int x = idx / R, ii = idx - x * R;
+                if (ii >= x) S.Ls[(size_t)x * RS + ii] = F[(kp + ii) + (size_t)(kp + x) * ld];
+            }
+            __syncthreads();
+        }
+        while (e < qe && e - kp < NB) {
+            const int k = e, t = k - kp;
+            if (fnext < s_forced[0] && step == s_forced[1 + fnext]) {
+                // the full-column test failed here in an earlier pass: delay (R1)
+                do_swap<NB>(S, RS, F, ld, q, kp, k, k, qe - 1, A.perm);
+                qe--;
+                fnext++;
+                step++;
+                continue;
+            }
+            if (tid < t) S.wrow[tid] = wform<NB>(S, RS, tid, k - kp);
+            __syncthreads();
+            MaxIdx mC{-1.0, INT_MAX};
+            double mR = 0.0, z1 = 0.0, z2 = 0.0;
+            {
+                const double* raw = S.Ls + (size_t)t * RS;
+                for (int i = k + tid; i < q; i += FT) {
+                    const int ii = i - kp;
+                    double v = raw[ii];
+                    for (int x = 0; x < t; ++x) v = fma(-S.Ls[(size_t)x * RS + ii], S.wrow[x], v);
+                    S.wk[ii] = v;
+                    if (i > k) {
+                        const double a = fabs(v);
+                        if (i < qe) mC = better(mC, MaxIdx{a, i});
+                        mR = fmax(mR, a);
+                    }
+                }
+            }
+            block_reduce(mC, mR, z1, z2, S.red);
+            const double gC = mC.v > 0.0 ? mC.v : 0.0;
+            const int r = mC.v >= 0.0 ? mC.i : k;
+            const double akk = fabs(S.wk[k - kp]);
+            if (akk == 0.0 && mR == 0.0) {
+                // FS part of column k is zero: a zero pivot if its CB part is
+                // zero too (k_check), else the unblocked rule delays it there
+                for (int i = k + tid; i < q; i += FT) S.Ls[(size_t)t * RS + (i - kp)] = 0.0;
+                if (tid == 0) {
+                    S.cs[t] = 0.0; S.co[t] = 0.0; S.oo[t] = 0; S.tp[t] = PK_ZERO;
+                    S.d1[t] = 0.0; S.d2[t] = 0.0; S.fa[t] = 0.0; S.fb[t] = 0.0; S.st[t] = step;
+                }
+                __syncthreads();
+                e++;
+                step++;
+                continue;
+            }
+            int kind = 1, j = k;
+            double rall = 0.0, gk = 0.0;
+            if (akk < kAlpha * gC) {
+                if (tid < t) S.wrowr[tid] = wform<NB>(S, RS, tid, r - kp);
+                __syncthreads();
+                double mc = 0.0, ma = 0.0, m3 = 0.0;
+                MaxIdx dm{-1.0, INT_MAX};
+                for (int i = k + tid; i < q; i += FT) {
+                    const int ii = i - kp;
+                    double v = i >= r ? F[i + (size_t)r * ld] : F[r + (size_t)i * ld];
+                    for (int x = 0; x < t; ++x) v = fma(-S.Ls[(size_t)x * RS + ii], S.wrowr[x], v);
+                    S.wr[ii] = v;
+                    if (i != r) {
+                        const double a = fabs(v);
+                        if (i < qe) mc = fmax(mc, a);
+                        if (i != k) { ma = fmax(ma, a); m3 = fmax(m3, fabs(S.wk[ii])); }
+                    }
+                }
+                block_reduce(dm, mc, ma, m3, S.red);
+                const double rho = mc;                       // includes |a_kr| = gC
+                rall = ma;                                   // column r, rows not in {k, r}
+                gk = m3;                                     // column k, rows not in {k, r}
+                const double arr = fabs(S.wr[r - kp]);
+                if (akk * rho >= kAlpha * gC * gC) { kind = 1; j = k; }
+                else if (arr >= kAlpha * rho) { kind = 1; j = r; }
+                else { kind = 2; j = r; }
+            }
+            if (kind == 2 && t + 2 > NB) break;             // no room for the 2x2 in this block
+            double fa = 0.0, fb = 0.0;
+            bool ok = true;
+            if (kind == 1 && j == k) fa = mR;
+            else if (kind == 1) fa = fmax(rall, gC);
+            else { fa = gk; fb = rall; }
+            if (!root) {
+                if (kind == 1) ok = fabs(j == k ? S.wk[k - kp] : S.wr[r - kp]) >= u * fa;
+                else {
+                    const double a11 = S.wk[k - kp], a21 = S.wk[r - kp], a22 = S.wr[r - kp];
+                    const double det = a11 * a22 - a21 * a21;
+                    if (det == 0.0) ok = false;
+                    else {
+                        const double ad = fabs(det);
+                        ok = (fabs(a22) * fa + fabs(a21) * fb) / ad <= 1.0 / u &&
+                             (fabs(a21) * fa + fabs(a11) * fb) / ad <= 1.0 / u;
+                    }
+                }
+            }
+            if (!ok) {                                      // fails on the FS rows already: delay
+                do_swap<NB>(S, RS, F, ld, q, kp, k, k, qe - 1, A.perm);
+                qe--;
+                step++;
+                continue;
+            }
+            if (kind == 1) {
+                double* w = S.wk;
+                if (j != k) {
+                    do_swap<NB>(S, RS, F, ld, q, kp, k + 1, k, j, A.perm);
+                    if (tid == 0) { const double x = S.wr[k - kp]; S.wr[k - kp] = S.wr[j - kp]; S.wr[j - kp] = x; }
+                    __syncthreads();
+                    w = S.wr;
+                }
+                const double d = w[k - kp];
+                const double dinv = 1.0 / d;
+                for (int i = k + 1 + tid; i < q; i += FT) S.Ls[(size_t)t * RS + (i - kp)] = w[i - kp] * dinv;
+                if (tid == 0) {
+                    S.cs[t] = d; S.co[t] = 0.0; S.oo[t] = 0; S.tp[t] = PK_1X1;
+                    S.d1[t] = d; S.d2[t] = 0.0; S.fa[t] = fa; S.fb[t] = 0.0; S.st[t] = step;
+                }
+                __syncthreads();
+                e += 1;
+                step++;
+            } else {
+                do_swap<NB>(S, RS, F, ld, q, kp, k + 2, k + 1, r, A.perm);
+                if (tid == 0) {
+                    double x = S.wk[k + 1 - kp]; S.wk[k + 1 - kp] = S.wk[r - kp]; S.wk[r - kp] = x;
+                    x = S.wr[k + 1 - kp]; S.wr[k + 1 - kp] = S.wr[r - kp]; S.wr[r - kp] = x;
+                }
+                __syncthreads();
+                const double d11 = S.wk[k - kp], d21 = S.wk[k + 1 - kp], d22 = S.wr[k + 1 - kp];
+                const double det = d11 * d22 - d21 * d21;
+                const double i11 = d22 / det, i21 = -d21 / det, i22 = d11 / det;
+                for (int i = k + 2 + tid; i < q; i += FT) {
+                    const double w1 = S.wk[i - kp], w2 = S.wr[i - kp];
+                    S.Ls[(size_t)t * RS + (i - kp)] = w1 * i11 + w2 * i21;
+                    S.Ls[(size_t)(t + 1) * RS + (i - kp)] = w1 * i21 + w2 * i22;
+                }
+                if (tid == 0) {
+                    S.cs[t] = d11; S.co[t] = d21; S.oo[t] = 1; S.tp[t] = PK_2X2A;
+                    S.cs[t + 1] = d22; S.co[t + 1] = d21; S.oo[t + 1] = -1; S.tp[t + 1] = PK_2X2B;
+                    S.d1[t] = d11; S.d2[t] = d21; S.fa[t] = fa; S.fb[t] = fb;
+                    S.d1[t + 1] = d22; S.d2[t + 1] = 0.0; S.fa[t + 1] = 0.0; S.fb[t + 1] = 0.0;
+                    S.st[t] = step; S.st[t + 1] = step;
+                }
+                __syncthreads();
+                e += 2;
+                step++;
+            }
+        }
+        // ---- commit the block: L (FS rows), D and the test record; FS trailing update
+        const int nbn = e - kp;
+        for (int t = warp; t < nbn; t += FT / 32) {
+            const int cpos = kp + t;
+            const int o = S.oo[t];
+            const int i1 = cpos + 1 + (o == 1 ? 1 : 0);
+            for (int i = i1 + lane; i < q; i += 32) F[i + (size_t)cpos * ld] = S.Ls[(size_t)t * RS + (i - kp)];
+            if (lane == 0) {
+                F[cpos + (size_t)cpos * ld] = S.d1[t];
+                if (o == 1) F[cpos + 1 + (size_t)cpos * ld] = 0.0;      // unit L: D's 2x2 coupling is in the record
+                A.d[cpos] = S.d1[t];
+                A.ds[cpos] = S.d2[t];
+                A.fa[cpos] = S.fa[t];
+                A.fb[cpos] = S.fb[t];
+                A.kind[cpos] = S.tp[t];
+                A.step[cpos] = S.st[t];
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        fst[0] = e; fst[1] = qe; fst[2] = step; fst[3] = fnext; fst[4] = kp; fst[5] = 1;   // update pending
+        if (e >= qe) nd_out[s] = q - e;
+    }
+}
+
+
+// ------------------------------------------------------------------ k_fsu
+// FS x FS trailing block [e, q)^2 (lower) -= L[:, kp:e] W[:, kp:e]^T after the
+// block [kp, e) committed by k_fsp, W = L D formed from the pivot record.
+// One CTA per 64 x 64 tile (tiles anchored at the current e).
+constexpr int UT = 128;
+constexpr int UK = 32;          // >= any NB
+constexpr int UPA = 64 + 4;     // = 4 (mod 16)
+
+__global__ void __launch_bounds__(UT) k_fsu(DevPlan P, const int4* __restrict__ items) {
+    __shared__ __align__(16) double As[UK][UPA];     // L[i, t]   (t-major)
+    __shared__ __align__(16) double Bs[64][UK + 4];  // W[j, t] = (L D)[j, t]
+    const int4 it = items[blockIdx.x];
+    const int s = it.x, I = it.y, J = it.z;
+    const int sh = blockIdx.y;
+    if (P.flag[(size_t)sh * P.nf + s] != FL_ACTIVE) return;
+    const int32_t* fst = P.fstate + ((size_t)sh * P.nf + s) * FSTATE_W;
+    if (fst[5] != 1) return;                              // no block committed since the last update
+    const int e = fst[0], kp = fst[4];
+    const int K = e - kp;
+    if (K <= 0) return;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int q = p + nd, ld = P.forder[s] + nd;
+    const int i0 = e + 64 * I, j0 = e + 64 * J;
+    if (i0 >= q) return;
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, tg = lane & 3;
+    for (int x = tid; x < UK * 64; x += UT) {
+        const int t = x >> 6, ii = x & 63;
+        const bool vt = t < K;
+        const int gi = i0 + ii, gj = j0 + ii;
+        As[t][ii] = (vt && gi < q) ? F[gi + (size_t)(kp + t) * ld] : 0.0;
+        double w = 0.0;
+        if (vt && gj < q) {
+            const int pos = kp + t, kd = A.kind[pos];
+            const double* Lj = F + gj;
+            if (kd == PK_1X1) w = Lj[(size_t)pos * ld] * A.d[pos];
+            else if (kd == PK_2X2A) w = Lj[(size_t)pos * ld] * A.d[pos] + Lj[(size_t)(pos + 1) * ld] * A.ds[pos];
+            else if (kd == PK_2X2B) w = Lj[(size_t)(pos - 1) * ld] * A.ds[pos - 1] + Lj[(size_t)pos * ld] * A.d[pos];
+        }
+        Bs[ii][t] = w;
+    }
+    __syncthreads();
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int k4 = 0; k4 < K; k4 += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb) a[mb] = As[k4 + tg][wm + 8 * mb + g];
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) b[nb] = Bs[wn + 8 * nb + g][k4 + tg];
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb], a[mb], b[nb]);
+    }
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = i0 + wm + 8 * mb + g;
+                const int j = j0 + wn + 8 * nb + 2 * tg + h;
+                if (i < q && j < q && i >= j) F[i + (size_t)j * ld] -= acc[mb][nb][h];
+            }
+}
+
+// ------------------------------------------------------------------ k_l21
+// W21 = A21 P^T L11^-T for 64 CB rows of one front; column maxima of W21.
+// L11[i,t] = 0 for t >= e (delayed columns have no pivot: their W21 column
+// is the fully updated CB part of the delayed column).
+__global__ void __launch_bounds__(LT) k_l21(DevPlan P, const int4* __restrict__ items) {
+    __shared__ __align__(16) double As[2][KC][APAD];
+    __shared__ __align__(16) double Bs[2][LB][BP];
+    static_assert(sizeof(double) * LR * (LB + 1) <= sizeof(double) * 2 * KC * APAD, "Sacc aliases As");
+    double (*Sacc)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(&As[0][0][0]);
+    __shared__ double Lbb[LB][LB + 1];
+    __shared__ int sperm[LB];
+    const int4 it = items[blockIdx.x];
+    const int s = it.x, I = it.y;
+    const int sh = blockIdx.y;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    if (nd < 0) return;
+    if (P.flag[(size_t)sh * P.nf + s] != FL_ACTIVE) return;
+    const int ndo = P.nd_out[(size_t)sh * P.nf + s];
+    if (ndo < 0) return;
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const int e = q - ndo;
+    const int r0 = q + I * LR;
+    if (r0 >= f) return;
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const int Q = P.cap[s] - c;
+    AuxRec A = aux_rec(P, sh, s, Q);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, tg = lane & 3;
+    const int wm = warp * 16;
+    for (int b0 = 0; b0 < q; b0 += LB) {
+        const int nbc = min(LB, q - b0);
+        const int K = min(b0, e);
+        double acc[2][4][2];
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+        if (K > 0) {
+            auto load = [&](int buf, int t0) {
+                for (int x = tid; x < KC * LR; x += LT) {
+                    const int ii = x / KC, tt = x - ii * KC;
+                    const int gi = r0 + ii, gt = t0 + tt;
+                    const bool v = gi < f && gt < K;
+                    cp_async8(&As[buf][tt][ii], F + (v ? (gt + (size_t)gi * ld) : 0), v);
+                }
+                for (int x = tid; x < KC * LB; x += LT) {
+                    const int tt = x / LB, jj = x - tt * LB;
+                    const int gt = t0 + tt;
+                    const bool v = jj < nbc && gt < K;
+                    cp_async8(&Bs[buf][jj][tt], F + (v ? ((b0 + jj) + (size_t)gt * ld) : 0), v);
+                }
+                cp_async_commit();
+            };
+            const int nk = (K + KC - 1) / KC;
+            load(0, 0);
+            for (int kc = 0; kc < nk; ++kc) {
+                const int buf = kc & 1;
+                if (kc + 1 < nk) {
+                    load(buf ^ 1, (kc + 1) * KC);
+                    cp_async_wait<1>();
+                } else {
+                    cp_async_wait<0>();
+                }
+                __syncthreads();
+#pragma unroll
+                for (int k4 = 0; k4 < KC; k4 += 4) {
+                    double a[2], b[4];
+#pragma unroll
+                    for (int mb = 0; mb < 2; ++mb) a[mb] = As[buf][k4 + tg][wm + 8 * mb + g];
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) b[nb] = Bs[buf][8 * nb + g][k4 + tg];
+#pragma unroll
+                    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+                        for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb], a[mb], b[nb]);
+                }
+                __syncthreads();
+            }
+        }
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) Sacc[wm + 8 * mb + g][8 * nb + 2 * tg + h] = acc[mb][nb][h];
+        // diagonal block of L11 (strict lower, columns < e only) and the permutation
+        for (int x = tid; x < LB * LB; x += LT) {
+            const int a = x / LB, b = x - a * LB;
+            double v = 0.0;
+            if (a < nbc && b < a && b0 + b < e) v = F[(b0 + a) + (size_t)(b0 + b) * ld];
+            Lbb[a][b] = v;
+        }
+        if (tid < LB) sperm[tid] = tid < nbc ? A.perm[b0 + tid] : 0;
+        __syncthreads();
+        if (tid < LR) {
+            const int i = r0 + tid;
+            const bool valid = i < f;
+            double xr[LB];
+#pragma unroll
+            for (int t = 0; t < LB; ++t) {
+                xr[t] = 0.0;
+                if (t < nbc) {
+                    double v = valid ? F[i + (size_t)sperm[t] * ld] : 0.0;
+                    v -= Sacc[tid][t];
+#pragma unroll
+                    for (int x = 0; x < t; ++x) v = fma(-xr[x], Lbb[t][x], v);
+                    xr[t] = v;
+                    if (valid) F[(b0 + t) + (size_t)i * ld] = v;
+                    double m = valid ? fabs(v) : 0.0;
+#pragma unroll
+                    for (int o2 = 16; o2 > 0; o2 >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o2));
+                    if (lane == 0 && m > 0.0 && b0 + t < e)
+                        atomicMax(&A.cm[b0 + t], (unsigned long long)__double_as_longlong(m));
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ k_check
+__global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restrict__ fronts) {
+    __shared__ int s_ok;
+        const int s = fronts[blockIdx.x];
+    const int sh = blockIdx.y;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    if (nd < 0) return;
+    int32_t* flag = P.flag + (size_t)sh * P.nf + s;
+    if (*flag != FL_ACTIVE) return;
+    __shared__ int s_fail;
+    const int ndo = P.nd_out[(size_t)sh * P.nf + s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const int e = q - ndo;
+    const bool root = c == 0;
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const int Q = P.cap[s] - c;
+    AuxRec A = aux_rec(P, sh, s, Q);
+    ShiftStat* st = P.stats + sh;
+    const double u = P.u;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        unsigned long long c_neg = 0, c_zero = 0, c_pos = 0, c_2x2 = 0;
+        double minpiv = DBL_MAX;
+        bool ok = true;
+        int tfail = -1;
+        for (int t = 0; t < e && ok;) {
+            const int kd = A.kind[t];
+            const double ca = root ? 0.0 : __longlong_as_double((long long)A.cm[t]);
+            const int t0 = t;
+            if (kd == PK_ZERO) {
+                ok = ca == 0.0;
+                c_zero++;
+                minpiv = 0.0;
+                t += 1;
+            } else if (kd == PK_1X1) {
+                const double d = A.d[t];
+                ok = root || fabs(d) >= u * fmax(A.fa[t], ca);
+                if (d < 0.0) c_neg++; else if (d > 0.0) c_pos++; else c_zero++;
+                minpiv = fmin(minpiv, fabs(d));
+                t += 1;
+            } else {
+                const double d11 = A.d[t], d21 = A.ds[t], d22 = A.d[t + 1];
+                const double det = d11 * d22 - d21 * d21;
+                if (!root) {
+                    const double cb = __longlong_as_double((long long)A.cm[t + 1]);
+                    const double gk = fmax(A.fa[t], ca), gr = fmax(A.fb[t], cb);
+                    if (det == 0.0) ok = false;
+                    else {
+                        const double ad = fabs(det);
+                        ok = (fabs(d22) * gk + fabs(d21) * gr) / ad <= 1.0 / u &&
+                             (fabs(d21) * gk + fabs(d11) * gr) / ad <= 1.0 / u;
+                    }
+                }
+                const double tt = (d11 / d21) * (d22 / d21) - 1.0;
+                if (tt < 0.0) { c_neg++; c_pos++; }
+                else if (tt > 0.0) { if (d11 < 0.0) c_neg += 2; else c_pos += 2; }
+                else { c_zero++; if (d11 + d22 < 0.0) c_neg++; else c_pos++; }
+                const double tr = 0.5 * (d11 + d22);
+                const double disc = sqrt(0.25 * (d11 - d22) * (d11 - d22) + d21 * d21);
+                const double big = fabs(tr) + disc;
+                minpiv = fmin(minpiv, big > 0.0 ? fabs(det) / big : 0.0);
+                c_2x2++;
+                t += 2;
+            }
+            if (!ok) tfail = t0;
+            if (!ok && P.debug)
+                printf("[kep] test fails: front %d shift %d pos %d kind %d d=%.3e ds=%.3e fa=%.3e fb=%.3e cm=%.3e cm1=%.3e\n",
+                       s, sh, t0, kd, A.d[t0], A.ds[t0], A.fa[t0], A.fb[t0], ca,
+                       __longlong_as_double((long long)A.cm[t0 + 1 < e ? t0 + 1 : t0]));
+        }
+        s_ok = ok;
+        s_fail = tfail;
+        if (!ok && P.debug)
+            printf("[kep] redo front %d shift %d: q=%d e=%d c=%d\n", s, sh, q, e, c);
+        if (ok) {
+            if (c_neg) atomicAdd(&st->n_neg, c_neg);
+            if (c_zero) atomicAdd(&st->n_zero, c_zero);
+            if (c_pos) atomicAdd(&st->n_pos, c_pos);
+            if (c_2x2) atomicAdd(&st->n_2x2, c_2x2);
+            if (ndo) atomicAdd(&st->n_delayed, (unsigned long long)ndo);
+            if (minpiv < DBL_MAX) atomic_min_pos_double(&st->minpiv_bits, minpiv);
+        }
+    }
+    __syncthreads();
+    if (!s_ok) {
+        // restore the assembled FS block; the unblocked kernel redoes this front
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int j = warp; j < q; j += FT / 32) {
+            for (int i = j + 1 + lane; i < q; i += 32) F[i + (size_t)j * ld] = F[j + (size_t)i * ld];
+            if (lane == 0) F[j + (size_t)j * ld] = A.diag[j];
+        }
+        if (tid == 0) {
+            int32_t* forced = P.forced + ((size_t)sh * P.nf + s) * (FMAX + 1);
+            const int nf_ = forced[0];
+            if (nf_ < FMAX) {                                // rerun the fast path, delaying there
+                forced[1 + nf_] = A.step[s_fail];
+                forced[0] = nf_ + 1;
+                *flag = FL_RERUN;
+                atomicAdd(P.pending, 1);
+            } else {
+                *flag = FL_REF;
+            }
+            atomicAdd(&st->n_redo, 1ull);
+        }
+        return;
+    }
+    if (tid == 0) *flag = FL_OK;
+    // D^-1 coefficients for k_schur (L21 = W21 D^-1 there), into the fa / fb slots:
+    // L[:, t] = W[:, t] * fa[t] + W[:, partner] * fb[t]
+    for (int t = tid; t < e; t += FT) {
+        const int kd = A.kind[t];
+        double ga = 0.0, gb = 0.0;
+        if (kd == PK_1X1) ga = 1.0 / A.d[t];
+        else if (kd == PK_2X2A || kd == PK_2X2B) {
+            const int a = kd == PK_2X2A ? t : t - 1;
+            const double d11 = A.d[a], d21 = A.ds[a], d22 = A.d[a + 1];
+            const double det = d11 * d22 - d21 * d21;
+            ga = (kd == PK_2X2A ? d22 : d11) / det;
+            gb = -d21 / det;
+        }
+        A.fa[t] = ga;
+        A.fb[t] = gb;
+    }
+    if (root || e == q) return;
+    // delayed columns [e, q): their updated CB rows (upper W21) to the lower part,
+    // where the parent's extend-add reads them
+    for (int idx = tid; idx < (q - e) * c; idx += FT) {
+        const int t = e + idx / c, i = q + idx % c;
+        F[i + (size_t)t * ld] = F[t + (size_t)i * ld];
+    }
+}
+
+}  // namespace
+
+constexpr size_t kFsSmemLimit = 200 * 1024;   // dynamic; + static shared stays under the 227 KB opt-in
+
+int fs_rows_pad(int qmax) { return ((qmax + 15) / 16) * 16 + 4; }
+
+// NB for a level whose fronts have at most qmax fully-summed columns (with
+// slack): the widest block whose shared memory fits; 0 = too large.
+int front_nb_for(int qmax) {
+    const int RS = fs_rows_pad(qmax);
+    const size_t lim = kFsSmemLimit;
+    if (fs_smem_bytes(32, RS) <= lim && qmax <= 384) return 32;
+    if (fs_smem_bytes(16, RS) <= lim) return 16;
+    if (fs_smem_bytes(8, RS) <= lim) return 8;
+    return 0;
+}
+
+int fs_iters(int qmax) {
+    const int nb = front_nb_for(qmax);
+    return nb > 1 ? (qmax + nb - 2) / (nb - 1) + 1 : 0;
+}
+
+void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    const int nb = front_nb_for(qmax);
+    const int RS = fs_rows_pad(qmax);
+    const size_t smem = fs_smem_bytes(nb, RS);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_fsp<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
+        cudaFuncSetAttribute(k_fsp<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
+        cudaFuncSetAttribute(k_fsp<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
+        attr = true;
+    }
+    const dim3 grid(nfronts, batch);
+    if (nb == 32) k_fsp<32><<<grid, FT, smem, st>>>(P, fronts, RS, mode);
+    else if (nb == 16) k_fsp<16><<<grid, FT, smem, st>>>(P, fronts, RS, mode);
+    else k_fsp<8><<<grid, FT, smem, st>>>(P, fronts, RS, mode);
+}
+
+void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
+    if (nitems <= 0) return;
+    k_fsu<<<dim3(nitems, batch), UT, 0, st>>>(P, items);
+}
+
+void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
+    if (nitems <= 0) return;
+    k_l21<<<dim3(nitems, batch), LT, 0, st>>>(P, items);
+}
+
+void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    k_check<<<dim3(nfronts, batch), FT, 0, st>>>(P, fronts);
+}
+
+}  // namespace kep

@@ -35,16 +35,17 @@ class _Opts(C.Structure):
 
 
 class _Profile(C.Structure):
-    _fields_ = [("ms", C.c_double * 4), ("launches", C.c_int64 * 4), ("schur_flops", C.c_double),
+    _fields_ = [("ms", C.c_double * 7), ("launches", C.c_int64 * 7), ("schur_flops", C.c_double),
                 ("factor_flops", C.c_double), ("shifts", C.c_int64), ("other_launches", C.c_int64)]
 
 
-KERNEL_CLASSES = ("assemble", "panel", "ref", "schur")
+KERNEL_CLASSES = ("assemble", "fs", "ref", "schur", "l21", "check", "fsu")
 
 
 class _Info(C.Structure):
     _fields_ = [("n_neg", C.c_int64), ("n_zero", C.c_int64), ("n_pos", C.c_int64), ("n_2x2", C.c_int64),
-                ("n_delayed", C.c_int64), ("min_abs_pivot", C.c_double), ("max_abs_entry", C.c_double)]
+                ("n_delayed", C.c_int64), ("min_abs_pivot", C.c_double), ("max_abs_entry", C.c_double),
+                ("n_redo", C.c_int64)]
 
 
 class _Analysis(C.Structure):
@@ -112,6 +113,7 @@ class InertiaInfo:
     n_delayed: int
     min_abs_pivot: float
     max_abs_entry: float
+    n_redo: int
 
 
 class Kep:
