@@ -538,7 +538,10 @@ kep_status kep_inertia_many(kep_ctx* c, int32_t m, const double* sigmas, int64_t
     KEP_CUDA(c, cudaSetDevice(c->device));
     int done = 0;
     while (done < m) {
-        const int b = std::min(m - done, c->batch_cap);
+        // equal-sized batches (16 shifts at capacity 12 run as 8 + 8, not 12 + 4)
+        const int left = m - done;
+        const int nbat = (left + c->batch_cap - 1) / c->batch_cap;
+        const int b = (left + nbat - 1) / nbat;
         kep_status st = run_batch(c, b, sigmas + done);
         if (st != KEP_OK) return st;
         const int got = std::min(b, c->batch_cap);     // a replan may shrink the batch

@@ -18,6 +18,7 @@
 // F[e:, e:] is exactly what the parent extend-adds.
 #include <cfloat>
 #include <climits>
+#include <cstdint>
 
 #include "device.cuh"
 
@@ -149,20 +150,40 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
         const int fc = P.forder[c] + nd_in[c];
         const int mc = ndo + P.ncb[c];
         const int ec = fc - mc;
-        const double* Fc = arena + P.arena_off[c];
-        const int32_t* rm = P.rmap + P.rmap_ptr[c];
+        const double* __restrict__ Fc = arena + P.arena_off[c];
+        double* __restrict__ Fp = F;
+        const int32_t* __restrict__ rm = P.rmap + P.rmap_ptr[c];
         const int dof = p + doff[c];
+        auto pos = [&](int x) -> int {                 // child CB index -> parent position
+            if (x < ndo) return dof + x;
+            const int r = rm[x - ndo];
+            return r < p ? r : r + nd;
+        };
+        constexpr int U = 4;                           // rows in flight per lane
         for (int j = warp; j < mc; j += nw) {
-            int pj;
-            if (j < ndo) pj = dof + j;
-            else { const int r = rm[j - ndo]; pj = r < p ? r : r + nd; }
-            const double* colc = Fc + (size_t)(ec + j) * fc + ec;
-            for (int i = j + lane; i < mc; i += 32) {
-                int pi;
-                if (i < ndo) pi = dof + i;
-                else { const int r = rm[i - ndo]; pi = r < p ? r : r + nd; }
-                const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
-                F[hi + (size_t)lo * ld] += colc[i];
+            const int pj = pos(j);
+            const double* __restrict__ colc = Fc + (size_t)(ec + j) * fc + ec;
+            for (int i0 = j; i0 < mc; i0 += 32 * U) {
+                double v[U];
+                size_t dst[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + lane + 32 * u;
+                    dst[u] = SIZE_MAX;
+                    v[u] = 0.0;
+                    if (i < mc) {
+                        const int pi = pos(i);
+                        const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
+                        dst[u] = hi + (size_t)lo * ld;
+                        v[u] = colc[i];
+                    }
+                }
+                double old[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) old[u] = dst[u] != SIZE_MAX ? Fp[dst[u]] : 0.0;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (dst[u] != SIZE_MAX) Fp[dst[u]] = old[u] + v[u];
             }
         }
         __syncthreads();

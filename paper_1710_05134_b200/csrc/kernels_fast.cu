@@ -41,8 +41,9 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
     // A operand: W21 rows with one halo column each side (2x2 partners),
     // turned into L21 = W21 D^-1 in shared memory; B operand: W21 rows.
     __shared__ __align__(16) double Aw[2][KC + 2][APAD];
-    __shared__ __align__(16) double Al[KC][APAD];
     __shared__ __align__(16) double Bs[2][ST][BPAD];
+    __shared__ double Ga[2][KC], Gb[2][KC];             // L[:, t] = W[:, t] Ga[t] + W[:, t + Go[t]] Gb[t]
+    __shared__ int Go[2][KC];
     const int4 it = items[blockIdx.x];          // (front, I, J, -)
     const int s = it.x, I = it.y, J = it.z;
     const int sh = blockIdx.y;
@@ -73,6 +74,18 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
             const bool v = gj < f && gt < e;
             cp_async8(&Bs[buf][jj][t], F + (v ? (gt + (size_t)gj * ld) : 0), v);
         }
+        if (tid < KC) {
+            const int t = t0 + tid;
+            double ga = 0.0, gb = 0.0;
+            int o = 0;
+            if (t < e) {
+                const int kd = A.kind[t];
+                ga = A.fa[t];
+                gb = A.fb[t];
+                o = kd == PK_2X2A ? 1 : (kd == PK_2X2B ? -1 : 0);
+            }
+            Ga[buf][tid] = ga; Gb[buf][tid] = gb; Go[buf][tid] = o;
+        }
         cp_async_commit();
     };
     double acc[4][4][2];
@@ -91,24 +104,15 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
             cp_async_wait<0>();
         }
         __syncthreads();
-        for (int x = tid; x < KC * ST; x += SCH_T) {  // L21 = W21 D^-1 (fa/fb hold the D^-1 coefficients)
-            const int tt = x / ST, i = x - tt * ST;
-            const int t = kc * KC + tt;
-            double v = 0.0;
-            if (t < e) {
-                const int kd = A.kind[t];
-                v = Aw[buf][tt + 1][i] * A.fa[t];
-                if (kd == PK_2X2A) v += Aw[buf][tt + 2][i] * A.fb[t];
-                else if (kd == PK_2X2B) v += Aw[buf][tt][i] * A.fb[t];
-            }
-            Al[tt][i] = v;
-        }
-        __syncthreads();
 #pragma unroll
         for (int k4 = 0; k4 < KC; k4 += 4) {
             double a[4], b[4];
+            const int tt = k4 + tg;
+            const double ga = Ga[buf][tt], gb = Gb[buf][tt];
+            const double* w0 = &Aw[buf][tt + 1][wm + g];
+            const double* w1 = &Aw[buf][tt + 1 + Go[buf][tt]][wm + g];
 #pragma unroll
-            for (int mb = 0; mb < 4; ++mb) a[mb] = Al[k4 + tg][wm + 8 * mb + g];
+            for (int mb = 0; mb < 4; ++mb) a[mb] = fma(w0[8 * mb], ga, w1[8 * mb] * gb);   // L21 = W21 D^-1
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb) b[nb] = Bs[buf][wn + 8 * nb + g][k4 + tg];
 #pragma unroll

@@ -648,22 +648,31 @@ __global__ void __launch_bounds__(LT) k_l21(DevPlan P, const int4* __restrict__ 
         if (tid < LR) {
             const int i = r0 + tid;
             const bool valid = i < f;
+            const double* __restrict__ Fi = F + i;
             double xr[LB];
 #pragma unroll
-            for (int t = 0; t < LB; ++t) {
-                xr[t] = 0.0;
-                if (t < nbc) {
-                    double v = valid ? F[i + (size_t)sperm[t] * ld] : 0.0;
-                    v -= Sacc[tid][t];
+            for (int t = 0; t < LB; ++t)                    // all loads first (no store can alias them)
+                xr[t] = (valid && t < nbc) ? Fi[(size_t)sperm[t] * ld] : 0.0;
 #pragma unroll
-                    for (int x = 0; x < t; ++x) v = fma(-xr[x], Lbb[t][x], v);
-                    xr[t] = v;
-                    if (valid) F[(b0 + t) + (size_t)i * ld] = v;
-                    double m = valid ? fabs(v) : 0.0;
+            for (int t = 0; t < LB; ++t) {
+                double v = xr[t] - Sacc[tid][t];
+#pragma unroll
+                for (int x = 0; x < t; ++x) v = fma(-xr[x], Lbb[t][x], v);
+                xr[t] = t < nbc ? v : 0.0;
+            }
+            if (valid) {
+                double* __restrict__ Wi = F + (size_t)i * ld + b0;
+#pragma unroll
+                for (int t = 0; t < LB; ++t)
+                    if (t < nbc) Wi[t] = xr[t];
+            }
+#pragma unroll
+            for (int t = 0; t < LB; ++t) {
+                if (t < nbc && b0 + t < e) {
+                    double m = valid ? fabs(xr[t]) : 0.0;
 #pragma unroll
                     for (int o2 = 16; o2 > 0; o2 >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o2));
-                    if (lane == 0 && m > 0.0 && b0 + t < e)
-                        atomicMax(&A.cm[b0 + t], (unsigned long long)__double_as_longlong(m));
+                    if (lane == 0 && m > 0.0) atomicMax(&A.cm[b0 + t], (unsigned long long)__double_as_longlong(m));
                 }
             }
         }
