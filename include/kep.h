@@ -172,6 +172,53 @@ KEP_API kep_status kep_inertia(kep_ctx* ctx, double sigma, int64_t* nu, kep_iner
 KEP_API kep_status kep_inertia_many(kep_ctx* ctx, int32_t m, const double* sigmas, int64_t* nus,
                             kep_status* per_shift, kep_inertia_info* infos);
 
+/* ---------------------------------------------------------------------------
+ * Retained factors and solves (SURVEY.md §8(f) row f1
+ * "the same factors serve the shift-and-invert Lanczos solves of stage 3").
+ * ------------------------------------------------------------------------- */
+typedef struct kep_factorization kep_factorization;
+
+typedef struct {
+    double sigma;                   /* the shift factorised */
+    int64_t nu;                     /* nu_sigma = n_neg of D */
+    kep_inertia_info inertia;
+    int64_t n;                      /* matrix order */
+    int64_t nnz_L;                  /* stored strictly-lower entries of L (structural) */
+    int64_t store_bytes;            /* device memory held by the factor */
+} kep_factor_stats;
+
+/* Factorise A - sigma B once and keep L, D and the permutation on the device:
+ *     P (A - sigma B) P^T = L D L^T,
+ * P = fill-reducing ordering composed with the Bunch-Kaufman / delayed-pivot
+ * permutation (the same kernels as kep_inertia).  The factor is owned by the
+ * caller, must not outlive ctx and is immutable (shareable for solves).
+ * Errors: KEP_ESINGULAR (some |pivot| <= tau_sing max|A - sigma B|; no factor
+ * is returned), KEP_ENOMEM, KEP_ECUDA, KEP_EINVAL (values not set). */
+KEP_API kep_status kep_factor(kep_ctx* ctx, double sigma, kep_factorization** out);
+
+/* Factor statistics (shift, nu, inertia, size of L). */
+KEP_API kep_status kep_factor_info(const kep_factorization* f, kep_factor_stats* out);
+
+/* x = (A - sigma B)^-1 b for nrhs right-hand sides (host, column-major,
+ * leading dimensions ldb, ldx >= n; x may alias b).  Multifrontal forward
+ * elimination, D^-1, back substitution.  Errors: KEP_EINVAL. */
+KEP_API kep_status kep_solve(const kep_factorization* f, int32_t nrhs, const double* b, int64_t ldb, double* x, int64_t ldx);
+
+/* Same for one right-hand side in device memory (n doubles each, dof order,
+ * may alias), enqueued on the ctx stream (not synchronised). */
+KEP_API kep_status kep_solve_dev(const kep_factorization* f, const double* b_dev, double* x_dev);
+
+/* Copy the factor to the host (testing, residual checks): perm[k] = dof
+ * eliminated k-th; d[k] = D[k,k]; dsub[k] = D[k+1,k] (nonzero only for the
+ * first column of a 2x2 block); L strictly lower in CSC (elimination order,
+ * unit diagonal implied, rows sorted): Lcolptr[n+1], Lrowidx/Lval[nnz_L].
+ * Lrowidx and Lval may be NULL to obtain Lcolptr (sizes) only. */
+KEP_API kep_status kep_factor_export(const kep_factorization* f, int64_t* perm, double* d, double* dsub,
+                                     int64_t* Lcolptr, int32_t* Lrowidx, double* Lval);
+
+/* Release a factor.  kep_destroy(ctx) releases the factors still alive on ctx. */
+KEP_API void kep_factor_destroy(kep_factorization* f);
+
 /* Analysis statistics (sizes, #nzf, flops per shift, memory). */
 KEP_API kep_status kep_get_analysis(const kep_ctx* ctx, kep_analysis_info* info);
 

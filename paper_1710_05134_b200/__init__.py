@@ -6,6 +6,6 @@ LDL^T-with-inertia of A - sigma B, plus the host symbolic analysis.
 ``kep`` is the ctypes binding; ``multisection`` is the host driver of stage 2
 (Alg. 1') generalised to P shifts per round over GPUs.
 """
-from .kep import Kep, KepError, lib, version, LIB_PATH
+from .kep import Factor, Kep, KepError, lib, version, LIB_PATH
 
-__all__ = ["Kep", "KepError", "lib", "version", "LIB_PATH"]
+__all__ = ["Factor", "Kep", "KepError", "lib", "version", "LIB_PATH"]

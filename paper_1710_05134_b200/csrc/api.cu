@@ -34,6 +34,8 @@ struct kep_ctx {
     // device arrays (static)
     int32_t *d_forder = nullptr, *d_npiv = nullptr, *d_ncb = nullptr, *d_cap = nullptr;
     int32_t *d_child_ptr = nullptr, *d_child_list = nullptr, *d_level_fronts = nullptr;
+    int32_t *d_piv_first = nullptr, *d_cb_ptr = nullptr, *d_cb_rows = nullptr;
+    int64_t *d_perm = nullptr, *d_iperm = nullptr;          // elimination position <-> dof
     int64_t *d_arena_off = nullptr, *d_asm_ptr = nullptr, *d_asm_src = nullptr, *d_rmap_ptr = nullptr;
     uint32_t* d_asm_rc = nullptr;
     int32_t* d_rmap = nullptr;
@@ -62,10 +64,36 @@ struct kep_ctx {
     std::vector<int64_t> uitem_off, uitem_cnt;
     std::vector<int> level_qmax;                // per level: max p + slack over its fast fronts
     std::vector<double> item_flops;             // per level: algorithmic a4 flops of its fast fronts
+    std::vector<kep_factorization*> factors;    // live factors (released by kep_destroy)
     // profiling
     kep_profile prof;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<int> ev_class;
+};
+
+// Retained factors of one shift.
+struct kep_factorization {
+    kep_ctx* ctx = nullptr;
+    double sigma = 0.0;
+    int64_t nu = 0;
+    kep_inertia_info info{};
+    // store (device) + offsets and level structure captured at creation
+    double* panel = nullptr;
+    int32_t* lab = nullptr;
+    double *d = nullptr, *ds = nullptr;
+    int32_t* kind = nullptr;
+    int4* hdr = nullptr;
+    int64_t *poff = nullptr, *loff = nullptr, *qoff = nullptr;
+    std::vector<int64_t> h_poff, h_loff, h_qoff;
+    std::vector<int> level_fmax;                 // per level: max front capacity (shared memory of the solves)
+    double *xw = nullptr, *bw = nullptr;         // work vectors (n)
+    int64_t panel_doubles = 0, lab_ints = 0, q_entries = 0;
+    kep::StorePlan plan() const {
+        kep::StorePlan T;
+        T.panel = panel; T.poff = poff; T.lab = lab; T.loff = loff;
+        T.d = d; T.ds = ds; T.kind = kind; T.qoff = qoff; T.hdr = hdr;
+        return T;
+    }
 };
 
 namespace {
@@ -227,6 +255,16 @@ kep_status upload_plan(kep_ctx* c) {
     KEP_CUDA(c, upload(&c->d_asm_rc, S.asm_rc));
     KEP_CUDA(c, upload(&c->d_rmap_ptr, S.rmap_ptr));
     KEP_CUDA(c, upload(&c->d_rmap, S.rmap));
+    {
+        std::vector<int32_t> pf(S.piv_first.begin(), S.piv_first.end());
+        std::vector<int32_t> cp(S.cb_ptr.begin(), S.cb_ptr.end());
+        std::vector<int32_t> cr(S.cb_rows.begin(), S.cb_rows.end());
+        KEP_CUDA(c, upload(&c->d_piv_first, pf));
+        KEP_CUDA(c, upload(&c->d_cb_ptr, cp));
+        KEP_CUDA(c, upload(&c->d_cb_rows, cr));
+        KEP_CUDA(c, upload(&c->d_perm, S.perm));
+        KEP_CUDA(c, upload(&c->d_iperm, S.iperm));
+    }
     KEP_CUDA(c, cudaMalloc(&c->d_a, std::max<int64_t>(S.nnz, 1) * sizeof(double)));
     KEP_CUDA(c, cudaMalloc(&c->d_b, std::max<int64_t>(S.nnz, 1) * sizeof(double)));
     kep_status r = build_lists(c);
@@ -258,6 +296,9 @@ DevPlan make_plan(kep_ctx* c) {
     P.child_ptr = c->d_child_ptr;
     P.child_list = c->d_child_list;
     P.level_fronts = c->d_level_fronts;
+    P.piv_first = c->d_piv_first;
+    P.cb_ptr = c->d_cb_ptr;
+    P.cb_rows = c->d_cb_rows;
     P.arena_off = c->d_arena_off;
     P.asm_ptr = c->d_asm_ptr;
     P.asm_rc = c->d_asm_rc;
@@ -284,10 +325,51 @@ DevPlan make_plan(kep_ctx* c) {
     return P;
 }
 
+void free_store(kep_factorization* k) {
+    void* ptrs[] = {k->panel, k->lab, k->d, k->ds, k->kind, k->hdr, k->poff, k->loff, k->qoff};
+    for (void* q : ptrs) cudaFree(q);
+    k->panel = nullptr; k->lab = nullptr; k->d = nullptr; k->ds = nullptr; k->kind = nullptr;
+    k->hdr = nullptr; k->poff = nullptr; k->loff = nullptr; k->qoff = nullptr;
+}
+
+// (Re)allocate the factor store for the current memory plan (capacities).
+kep_status prepare_store(kep_ctx* c, kep_factorization* k) {
+    free_store(k);
+    const Symbolic& S = c->sym;
+    k->h_poff.assign(S.nf, 0); k->h_loff.assign(S.nf, 0); k->h_qoff.assign(S.nf, 0);
+    int64_t po = 0, lo = 0, qo = 0;
+    for (int64_t s = 0; s < S.nf; ++s) {
+        const int64_t cap = S.capacity[s], Q = cap - S.ncb[s];
+        k->h_poff[s] = po; k->h_loff[s] = lo; k->h_qoff[s] = qo;
+        po += cap * Q; lo += cap; qo += Q;
+    }
+    k->panel_doubles = po; k->lab_ints = lo; k->q_entries = qo;
+    KEP_CUDA(c, cudaMalloc(&k->panel, std::max<int64_t>(po, 1) * sizeof(double)));
+    KEP_CUDA(c, cudaMalloc(&k->lab, std::max<int64_t>(lo, 1) * sizeof(int32_t)));
+    KEP_CUDA(c, cudaMalloc(&k->d, std::max<int64_t>(qo, 1) * sizeof(double)));
+    KEP_CUDA(c, cudaMalloc(&k->ds, std::max<int64_t>(qo, 1) * sizeof(double)));
+    KEP_CUDA(c, cudaMalloc(&k->kind, std::max<int64_t>(qo, 1) * sizeof(int32_t)));
+    KEP_CUDA(c, cudaMalloc(&k->hdr, std::max<int64_t>(S.nf, 1) * sizeof(int4)));
+    KEP_CUDA(c, upload(&k->poff, k->h_poff));
+    KEP_CUDA(c, upload(&k->loff, k->h_loff));
+    KEP_CUDA(c, upload(&k->qoff, k->h_qoff));
+    const int nl = (int)S.level_ptr.size() - 1;
+    k->level_fmax.assign(nl, 0);
+    for (int L = 0; L < nl; ++L)
+        for (int x = S.level_ptr[L]; x < S.level_ptr[L + 1]; ++x)
+            k->level_fmax[L] = std::max(k->level_fmax[L], (int)S.capacity[S.level_fronts[x]]);
+    return KEP_OK;
+}
+
 // One batch of `m` shifts through every level.  Fills c->h_stats[0..m).
-kep_status run_batch(kep_ctx* c, int m, const double* sigmas) {
+// keep != NULL (m == 1): the factors are copied into keep's store level by level.
+kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization* keep = nullptr) {
     for (int attempt = 0; attempt < 8; ++attempt) {
         if (m > c->batch_cap) return fail(c, KEP_EINVAL, "internal: batch larger than capacity");
+        if (keep) {
+            kep_status r = prepare_store(c, keep);
+            if (r != KEP_OK) return r;
+        }
         KEP_CUDA(c, cudaMemcpyAsync(c->d_sigma, sigmas, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
         kep::launch_reset_stats(c->d_stats, m, c->stream);
         c->prof.other_launches += 1;
@@ -364,6 +446,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas) {
                 mark(KEP_K_REF, false);
                 c->prof.launches[KEP_K_REF]++;
             }
+            if (keep) kep::launch_store(P, keep->plan(), c->d_level_fronts + b, nfl, c->stream);
             if (c->item_cnt[L]) {
                 mark(KEP_K_SCHUR, true);
                 kep::launch_schur(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
@@ -579,6 +662,174 @@ kep_status kep_inertia(kep_ctx* c, double sigma, int64_t* nu, kep_inertia_info* 
     return per;
 }
 
+kep_status kep_factor(kep_ctx* c, double sigma, kep_factorization** out) {
+    if (!c || !out) return fail(c, KEP_EINVAL, "null argument");
+    *out = nullptr;
+    if (!c->have_device) return fail(c, KEP_ENODEVICE, "no CUDA device");
+    if (!c->values_set) return fail(c, KEP_EINVAL, "kep_set_values must precede kep_factor");
+    KEP_CUDA(c, cudaSetDevice(c->device));
+    kep_factorization* k = new (std::nothrow) kep_factorization();
+    if (!k) return fail(c, KEP_ENOMEM, "host allocation failed");
+    k->ctx = c;
+    k->sigma = sigma;
+    kep_status st = run_batch(c, 1, &sigma, k);
+    if (st != KEP_OK) { kep_factor_destroy(k); return st; }
+    const ShiftStat& S = c->h_stats[0];
+    const double minpiv = bits_to_double(S.minpiv_bits), smax = bits_to_double(S.smax_bits);
+    kep_inertia_info& I = k->info;
+    I.n_neg = (int64_t)S.n_neg; I.n_zero = (int64_t)S.n_zero; I.n_pos = (int64_t)S.n_pos;
+    I.n_2x2 = (int64_t)S.n_2x2; I.n_delayed = (int64_t)S.n_delayed;
+    I.min_abs_pivot = minpiv >= DBL_MAX ? 0.0 : minpiv;
+    I.max_abs_entry = smax;
+    I.n_redo = (int64_t)S.n_redo;
+    k->nu = I.n_neg;
+    if (S.n_zero > 0 || minpiv <= c->opts.tau_sing * smax) {
+        kep_factor_destroy(k);
+        return fail(c, KEP_ESINGULAR, "A - sigma B is numerically singular at this shift");
+    }
+    const int64_t n = c->sym.n;
+    cudaError_t e1 = cudaMalloc(&k->xw, std::max<int64_t>(n, 1) * sizeof(double));
+    cudaError_t e2 = cudaMalloc(&k->bw, std::max<int64_t>(n, 1) * sizeof(double));
+    if (e1 != cudaSuccess || e2 != cudaSuccess) { kep_factor_destroy(k); return fail(c, KEP_ENOMEM, "cudaMalloc failed"); }
+    c->factors.push_back(k);
+    *out = k;
+    return KEP_OK;
+}
+
+kep_status kep_factor_info(const kep_factorization* k, kep_factor_stats* out) {
+    if (!k || !out) return KEP_EINVAL;
+    out->sigma = k->sigma;
+    out->nu = k->nu;
+    out->inertia = k->info;
+    out->n = k->ctx->sym.n;
+    std::vector<int4> hdr(k->ctx->sym.nf);
+    if (cudaMemcpy(hdr.data(), k->hdr, sizeof(int4) * hdr.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return KEP_ECUDA;
+    int64_t nnz = 0;
+    for (const int4& h : hdr)
+        for (int t = 0; t < h.x; ++t) nnz += h.y - t - 1;
+    out->nnz_L = nnz;
+    out->store_bytes = k->panel_doubles * 8 + k->lab_ints * 4 + k->q_entries * 20;
+    return KEP_OK;
+}
+
+// x = S^-1 b on the device, positions space: b_dev / x_dev in dof order (n doubles each).
+kep_status kep_solve_dev(const kep_factorization* k, const double* b_dev, double* x_dev) {
+    if (!k || !b_dev || !x_dev) return KEP_EINVAL;
+    kep_ctx* c = k->ctx;
+    KEP_CUDA(c, cudaSetDevice(c->device));
+    const Symbolic& S = c->sym;
+    const int nl = (int)S.level_ptr.size() - 1;
+    for (int L = 0; L < nl; ++L)
+        if (k->level_fmax[L] > kep::solve_max_front())
+            return fail(c, KEP_EINVAL, "front too large for the solve kernels");
+    kep::launch_gather(b_dev, c->d_perm, k->xw, S.n, c->stream);          // to elimination positions
+    const kep::StorePlan T = k->plan();
+    for (int L = 0; L < nl; ++L)
+        kep::launch_fwd(T, c->d_level_fronts + S.level_ptr[L], S.level_ptr[L + 1] - S.level_ptr[L], k->level_fmax[L],
+                        k->xw, c->stream);
+    for (int L = nl - 1; L >= 0; --L)
+        kep::launch_bwd(T, c->d_level_fronts + S.level_ptr[L], S.level_ptr[L + 1] - S.level_ptr[L], k->level_fmax[L],
+                        k->xw, c->stream);
+    kep::launch_gather(k->xw, c->d_iperm, x_dev, S.n, c->stream);         // back to dofs
+    KEP_CUDA(c, cudaGetLastError());
+    return KEP_OK;
+}
+
+kep_status kep_solve(const kep_factorization* k, int32_t nrhs, const double* b, int64_t ldb, double* x, int64_t ldx) {
+    if (!k || (nrhs > 0 && (!b || !x))) return KEP_EINVAL;
+    kep_ctx* c = k->ctx;
+    const int64_t n = c->sym.n;
+    if (nrhs < 0 || ldb < n || ldx < n) return fail(c, KEP_EINVAL, "nrhs < 0 or leading dimension < n");
+    KEP_CUDA(c, cudaSetDevice(c->device));
+    for (int32_t r = 0; r < nrhs; ++r) {
+        KEP_CUDA(c, cudaMemcpyAsync(k->bw, b + (size_t)r * ldb, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        kep_status st = kep_solve_dev(k, k->bw, k->bw);
+        if (st != KEP_OK) return st;
+        KEP_CUDA(c, cudaMemcpyAsync(x + (size_t)r * ldx, k->bw, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    KEP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return KEP_OK;
+}
+
+kep_status kep_factor_export(const kep_factorization* k, int64_t* perm, double* d, double* dsub, int64_t* Lcolptr,
+                             int32_t* Lrowidx, double* Lval) {
+    if (!k || !perm || !d || !dsub || !Lcolptr) return KEP_EINVAL;
+    kep_ctx* c = k->ctx;
+    const Symbolic& S = c->sym;
+    const int64_t n = S.n, nf = S.nf;
+    std::vector<int4> hdr(nf);
+    std::vector<int32_t> lab(k->lab_ints), kind(k->q_entries);
+    std::vector<double> dd(k->q_entries), ds(k->q_entries);
+    KEP_CUDA(c, cudaMemcpy(hdr.data(), k->hdr, sizeof(int4) * nf, cudaMemcpyDeviceToHost));
+    KEP_CUDA(c, cudaMemcpy(lab.data(), k->lab, sizeof(int32_t) * lab.size(), cudaMemcpyDeviceToHost));
+    KEP_CUDA(c, cudaMemcpy(kind.data(), k->kind, sizeof(int32_t) * kind.size(), cudaMemcpyDeviceToHost));
+    KEP_CUDA(c, cudaMemcpy(dd.data(), k->d, sizeof(double) * dd.size(), cudaMemcpyDeviceToHost));
+    KEP_CUDA(c, cudaMemcpy(ds.data(), k->ds, sizeof(double) * ds.size(), cudaMemcpyDeviceToHost));
+    // elimination index of every variable (fronts in postorder, eliminated positions in order)
+    std::vector<int64_t> elim_of(n, -1);
+    int64_t kk = 0;
+    for (int64_t s = 0; s < nf; ++s)
+        for (int t = 0; t < hdr[s].x; ++t) {
+            const int32_t v = lab[k->h_loff[s] + t];
+            if (v < 0 || v >= n || elim_of[v] >= 0) return fail(c, KEP_ECUDA, "inconsistent factor labels");
+            elim_of[v] = kk;
+            perm[kk] = S.perm[v];
+            const int64_t qi = k->h_qoff[s] + t;
+            d[kk] = dd[qi];
+            dsub[kk] = kind[qi] == kep::PK_2X2A ? ds[qi] : 0.0;
+            ++kk;
+        }
+    if (kk != n) return fail(c, KEP_ECUDA, "factor does not eliminate every variable");
+    // column counts, then entries (structural, rows sorted)
+    Lcolptr[0] = 0;
+    for (int64_t s = 0; s < nf; ++s)
+        for (int t = 0; t < hdr[s].x; ++t) {
+            const int64_t col = elim_of[lab[k->h_loff[s] + t]];
+            Lcolptr[col + 1] = hdr[s].y - t - 1;
+        }
+    for (int64_t j = 0; j < n; ++j) Lcolptr[j + 1] += Lcolptr[j];
+    if (!Lrowidx || !Lval) return KEP_OK;                    // sizes only
+    std::vector<double> col;
+    std::vector<std::pair<int64_t, double>> ent;
+    for (int64_t s = 0; s < nf; ++s) {
+        const int e = hdr[s].x, f = hdr[s].y;
+        if (e == 0) continue;
+        col.resize((size_t)f * e);
+        KEP_CUDA(c, cudaMemcpy(col.data(), k->panel + k->h_poff[s], sizeof(double) * col.size(), cudaMemcpyDeviceToHost));
+        for (int t = 0; t < e; ++t) {
+            const int64_t j = elim_of[lab[k->h_loff[s] + t]];
+            ent.clear();
+            for (int i = t + 1; i < f; ++i) ent.emplace_back(elim_of[lab[k->h_loff[s] + i]], col[(size_t)t * f + i]);
+            std::sort(ent.begin(), ent.end());
+            int64_t w = Lcolptr[j];
+            for (auto& pr : ent) {
+                if (pr.first <= j) return fail(c, KEP_ECUDA, "factor entry above the diagonal");
+                Lrowidx[w] = (int32_t)pr.first;
+                Lval[w] = pr.second;
+                ++w;
+            }
+        }
+    }
+    return KEP_OK;
+}
+
+void kep_factor_destroy(kep_factorization* k) {
+    if (!k) return;
+    if (k->ctx) {
+        auto& v = k->ctx->factors;
+        v.erase(std::remove(v.begin(), v.end(), k), v.end());
+    }
+    if (k->ctx && k->ctx->have_device) {
+        cudaSetDevice(k->ctx->device);
+        cudaStreamSynchronize(k->ctx->stream);
+        free_store(k);
+        cudaFree(k->xw);
+        cudaFree(k->bw);
+    }
+    delete k;
+}
+
 kep_status kep_get_analysis(const kep_ctx* c, kep_analysis_info* I) {
     if (!c || !I) return KEP_EINVAL;
     const Symbolic& S = c->sym;
@@ -633,6 +884,7 @@ kep_status kep_get_fronts(const kep_ctx* c, int64_t* first, int64_t* parent, int
 
 void kep_destroy(kep_ctx* c) {
     if (!c) return;
+    while (!c->factors.empty()) kep_factor_destroy(c->factors.back());
     if (c->have_device) {
         cudaSetDevice(c->device);
         if (c->stream) cudaStreamSynchronize(c->stream);
@@ -640,7 +892,8 @@ void kep_destroy(kep_ctx* c) {
         void* ptrs[] = {c->d_forder, c->d_npiv, c->d_ncb, c->d_cap, c->d_child_ptr, c->d_child_list,
                         c->d_level_fronts, c->d_arena_off, c->d_asm_ptr, c->d_asm_src, c->d_rmap_ptr,
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
-                        c->d_litems, c->d_aux_off, c->d_uitems};
+                        c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
+                        c->d_cb_rows, c->d_perm, c->d_iperm};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -26,6 +26,9 @@ struct DevPlan {
     const int32_t* child_ptr;
     const int32_t* child_list;
     const int32_t* level_fronts;
+    const int32_t* piv_first;    // [nf+1] first pivot position of each front
+    const int32_t* cb_ptr;       // [nf+1]
+    const int32_t* cb_rows;      // CB row positions of each front
     const int64_t* arena_off;    // doubles, within one shift's arena
     const int64_t* asm_ptr;
     const uint32_t* asm_rc;      // (lrow << 16) | lcol
@@ -66,6 +69,7 @@ struct AuxRec {
     double *diag, *d, *ds, *fa, *fb;
     unsigned long long* cm;      // CB column maxima of W21 (positive-double bits)
     int *kind, *perm, *step;
+    int* label;                  // assembly-order variable (elimination position) of each FS position
 };
 
 __device__ __forceinline__ AuxRec aux_rec(const DevPlan& P, int sh, int s, int Q) {
@@ -76,6 +80,7 @@ __device__ __forceinline__ AuxRec aux_rec(const DevPlan& P, int sh, int s, int Q
     A.kind = (int*)(b + 6 * Q);
     A.perm = A.kind + Q;
     A.step = (int*)(b + 7 * Q);
+    A.label = A.step + Q;
     return A;
 }
 
@@ -86,11 +91,30 @@ __device__ __forceinline__ void atomic_min_pos_double(unsigned long long* addr, 
     atomicMin(addr, (unsigned long long)__double_as_longlong(v));
 }
 
-// Launchers (kernels.cu, kernels_front.cu, kernels_fast.cu)
+// Retained factors of one shift (kep_factor; kernels_solve.cu).  Per front s:
+// panel f_s x e_s (ld f_s) at panel + poff[s], row labels at lab + loff[s],
+// D / kind at qoff[s] (same entry offsets as the aux records), hdr = (e, f, q, path).
+struct StorePlan {
+    double* panel;
+    const int64_t* poff;
+    int32_t* lab;
+    const int64_t* loff;
+    double* d;
+    double* ds;
+    int32_t* kind;
+    const int64_t* qoff;
+    int4* hdr;
+};
+
+// Launchers (kernels.cu, kernels_front.cu, kernels_fast.cu, kernels_solve.cu)
 void launch_assemble(const DevPlan& P, int lvl_begin, int nfronts, int batch, cudaStream_t st);
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st);
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 int fs_iters(int qmax);               // k_fsp launches that finish every front of a level
+void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, cudaStream_t st);
+void launch_fwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
+void launch_bwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
+int solve_max_front();
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 int front_nb_for(int qmax);           // block width for a level (0: too large, use the reference kernel)

@@ -128,6 +128,18 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
     const int nd = s_nd, p = P.npiv[s], ld = P.forder[s] + nd;
     double* F = arena + P.arena_off[s];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAsmThreads / 32;
+    {   // labels of the FS positions: own pivots, then each child's delayed variables
+        const AuxRec A = aux_rec(P, sh, s, P.cap[s] - P.ncb[s]);
+        for (int i = threadIdx.x; i < p; i += kAsmThreads) A.label[i] = P.piv_first[s] + i;
+        for (int q = c0; q < c1; ++q) {
+            const int c = P.child_list[q];
+            const int ndo = nd_out[c];
+            if (ndo <= 0) continue;
+            const AuxRec C = aux_rec(P, sh, c, P.cap[c] - P.ncb[c]);
+            const int ec = P.npiv[c] + nd_in[c] - ndo;
+            for (int j = threadIdx.x; j < ndo; j += kAsmThreads) A.label[p + doff[c] + j] = C.label[C.perm[ec + j]];
+        }
+    }
     for (int j = warp; j < ld; j += nw)
         for (int i = j + lane; i < ld; i += 32) F[i + (size_t)j * ld] = 0.0;
     __syncthreads();
@@ -227,6 +239,10 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
     const int f = P.forder[s] + nd, q = p + nd, ld = f;
     const bool root = (c == 0);
     const double u = P.u;
+    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
+    if (threadIdx.x == 0) P.flag[(size_t)sh * P.nf + s] = FL_REF;      // factor layout: all of L in the lower part
+    for (int i = threadIdx.x; i < q; i += kRefThreads) A.perm[i] = i;
+    __syncthreads();
     __shared__ MaxIdx s_mi[32];
     __shared__ double s_red[32];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kRefThreads / 32;
@@ -249,6 +265,7 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
         const int r = mC.v >= 0.0 ? mC.i : k;
         const double akk = fabs(F[k + (size_t)k * ld]);
         if (akk == 0.0 && gR == 0.0) {          // zero column: exact zero pivot
+            if (threadIdx.x == 0) { A.kind[k] = PK_ZERO; A.d[k] = 0.0; A.ds[k] = 0.0; }
             c_zero++;
             minpiv = 0.0;
             e++;
@@ -299,6 +316,7 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
             }
             __syncthreads();                      // every thread has read the pivot entries
             if (!ok) {                            // delay column k to the parent
+                if (threadIdx.x == 0) { const int x = A.perm[k]; A.perm[k] = A.perm[qe - 1]; A.perm[qe - 1] = x; }
                 sym_swap(F, ld, f, k, qe - 1);
                 qe--;
                 c_del++;
@@ -307,8 +325,10 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
         }
         if (root) __syncthreads();                // (non-root fronts synchronised above)
         if (kind == 1) {
+            if (threadIdx.x == 0 && j != k) { const int x = A.perm[k]; A.perm[k] = A.perm[j]; A.perm[j] = x; }
             sym_swap(F, ld, f, k, j);
             const double d = F[k + (size_t)k * ld];
+            if (threadIdx.x == 0) { A.kind[k] = PK_1X1; A.d[k] = d; A.ds[k] = 0.0; }
             const double dinv = 1.0 / d;
             for (int jj = k + 1 + warp; jj < f; jj += nw) {
                 const double wj = F[jj + (size_t)k * ld] * dinv;
@@ -323,8 +343,13 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
             minpiv = fmin(minpiv, fabs(d));
             e += 1;
         } else {
+            if (threadIdx.x == 0 && r != k + 1) { const int x = A.perm[k + 1]; A.perm[k + 1] = A.perm[r]; A.perm[r] = x; }
             sym_swap(F, ld, f, k + 1, r);
             const double d11 = F[k + (size_t)k * ld], d21 = F[k + 1 + (size_t)k * ld], d22 = F[k + 1 + (size_t)(k + 1) * ld];
+            if (threadIdx.x == 0) {
+                A.kind[k] = PK_2X2A; A.d[k] = d11; A.ds[k] = d21;
+                A.kind[k + 1] = PK_2X2B; A.d[k + 1] = d22; A.ds[k + 1] = 0.0;
+            }
             const double det = d11 * d22 - d21 * d21;
             const double i11 = d22 / det, i21 = -d21 / det, i22 = d11 / det;
             const double* col1 = F + (size_t)k * ld;

@@ -1,0 +1,169 @@
+// kernels_solve.cu — SURVEY.md §8(f) row f1: retained factors and the
+// supernodal (multifrontal) triangular solves with them.
+//
+// kep_factor keeps, per front s, the panel of its eliminated columns
+// (f_s x e_s, column-major, ld = f_s; unit lower L, zero at the in-pair entry
+// of a 2x2 block), the labels of its rows (elimination positions of the
+// variables: FS positions after pivoting, then the CB rows) and D.  With
+// S = P Q (A - sigma B) Q^T P^T = L D L^T  (Alg. 1' line 3), a
+// solve S y = b is
+//   forward  (postorder levels):  y_e = L11^-1 b_e per front, CB/delayed rows
+//                                 receive -L21 y_e (scatter-add to the parent side),
+//            then z_e = D^-1 y_e;
+//   backward (reverse levels):    x_e = L11^-T (z_e - L21^T x_rest).
+// These are the shift-and-invert solves of stage 3 (Alg. 3)
+// and of the stage-1 B-solves.
+#include <cstdint>
+
+#include "device.cuh"
+
+namespace kep {
+
+namespace {
+
+constexpr int ST_T = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double r = 0.0;
+#pragma unroll
+    for (int q = 0; q < ST_T / 32; ++q) r += red[q];
+    return r;
+}
+
+// Copy the factor panel of each front of a level (shift 0 of the batch) into
+// the factor store.  Fast-path fronts keep W21 in the upper part: L21 = W21 D^-1
+// (coefficients left in fa / fb by k_check); unblocked fronts keep L in the lower part.
+__global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const int32_t* __restrict__ fronts) {
+    const int s = fronts[blockIdx.x];
+    const int nd = P.nd_in[s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const int e = q - P.nd_out[s];
+    const int flag = P.flag[s];
+    const double* F = P.arena + P.arena_off[s];
+    const AuxRec A = aux_rec(P, 0, s, P.cap[s] - c);
+    double* panel = T.panel + T.poff[s];
+    int* lab = T.lab + T.loff[s];
+    const int64_t qo = T.qoff[s];
+    if (threadIdx.x == 0) T.hdr[s] = make_int4(e, f, q, flag);
+    for (int i = threadIdx.x; i < f; i += ST_T)
+        lab[i] = i < q ? A.label[A.perm[i]] : P.cb_rows[P.cb_ptr[s] + (i - q)];
+    for (int t = threadIdx.x; t < e; t += ST_T) {
+        T.d[qo + t] = A.d[t];
+        T.ds[qo + t] = A.ds[t];
+        T.kind[qo + t] = A.kind[t];
+    }
+    for (int t = 0; t < e; ++t) {
+        const int kd = A.kind[t];
+        const int o = kd == PK_2X2A ? 1 : (kd == PK_2X2B ? -1 : 0);
+        double* col = panel + (size_t)t * ld;
+        for (int i = threadIdx.x; i < f; i += ST_T) {
+            double v = 0.0;
+            if (i > t && !(kd == PK_2X2A && i == t + 1)) {
+                if (i < q || flag == FL_REF) v = F[i + (size_t)t * ld];
+                else v = F[t + (size_t)i * ld] * A.fa[t] + (o ? F[(t + o) + (size_t)i * ld] * A.fb[t] : 0.0);
+            }
+            if (kd == PK_ZERO) v = 0.0;
+            col[i] = v;
+        }
+    }
+}
+
+// forward elimination and D^-1 for the fronts of one level; x in elimination positions
+__global__ void __launch_bounds__(ST_T) k_fwd(StorePlan T, const int32_t* __restrict__ fronts, double* __restrict__ x) {
+    extern __shared__ double y[];
+    const int s = fronts[blockIdx.x];
+    const int4 h = T.hdr[s];
+    const int e = h.x, f = h.y;
+    const double* L = T.panel + T.poff[s];
+    const int* lab = T.lab + T.loff[s];
+    const int64_t qo = T.qoff[s];
+    for (int i = threadIdx.x; i < f; i += ST_T) y[i] = i < e ? x[lab[i]] : 0.0;
+    __syncthreads();
+    for (int t = 0; t < e; ++t) {
+        const double yt = y[t];
+        const double* col = L + (size_t)t * f;
+        for (int i = t + 1 + threadIdx.x; i < f; i += ST_T) y[i] = fma(-col[i], yt, y[i]);
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < e; t += ST_T) {
+        const int kd = T.kind[qo + t];
+        double z = 0.0;
+        if (kd == PK_1X1) z = y[t] / T.d[qo + t];
+        else if (kd == PK_2X2A || kd == PK_2X2B) {
+            const int a = kd == PK_2X2A ? t : t - 1;
+            const double d11 = T.d[qo + a], d21 = T.ds[qo + a], d22 = T.d[qo + a + 1];
+            const double det = d11 * d22 - d21 * d21;
+            z = kd == PK_2X2A ? (d22 * y[a] - d21 * y[a + 1]) / det : (d11 * y[a + 1] - d21 * y[a]) / det;
+        }
+        x[lab[t]] = z;
+    }
+    for (int i = e + threadIdx.x; i < f; i += ST_T) atomicAdd(&x[lab[i]], y[i]);
+}
+
+// back substitution for the fronts of one level (levels top-down)
+__global__ void __launch_bounds__(ST_T) k_bwd(StorePlan T, const int32_t* __restrict__ fronts, double* __restrict__ x) {
+    extern __shared__ double xs[];
+    __shared__ double red[ST_T / 32];
+    const int s = fronts[blockIdx.x];
+    const int4 h = T.hdr[s];
+    const int e = h.x, f = h.y;
+    const double* L = T.panel + T.poff[s];
+    const int* lab = T.lab + T.loff[s];
+    for (int i = threadIdx.x; i < f; i += ST_T) xs[i] = x[lab[i]];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < e; t += ST_T / 32) {            // z_t - L21[:, t] . x_rest
+        const double* col = L + (size_t)t * f;
+        double a = 0.0;
+        for (int i = e + lane; i < f; i += 32) a = fma(col[i], xs[i], a);
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) xs[t] -= a;
+    }
+    __syncthreads();
+    for (int t = e - 1; t >= 0; --t) {                      // L11^-T
+        const double* col = L + (size_t)t * f;
+        double a = 0.0;
+        for (int i = t + 1 + threadIdx.x; i < e; i += ST_T) a = fma(col[i], xs[i], a);
+        a = block_sum(a, red);
+        if (threadIdx.x == 0) xs[t] -= a;
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < e; t += ST_T) x[lab[t]] = xs[t];
+}
+
+}  // namespace
+
+void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    k_store<<<nfronts, ST_T, 0, st>>>(P, T, fronts);
+}
+
+static void set_smem_attr() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    done = true;
+}
+
+int solve_max_front() { return 200 * 1024 / 8; }
+
+void launch_fwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    set_smem_attr();
+    k_fwd<<<nfronts, ST_T, (size_t)fmax * sizeof(double), st>>>(T, fronts, x);
+}
+
+void launch_bwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    set_smem_attr();
+    k_bwd<<<nfronts, ST_T, (size_t)fmax * sizeof(double), st>>>(T, fronts, x);
+}
+
+}  // namespace kep

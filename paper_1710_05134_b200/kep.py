@@ -57,6 +57,11 @@ class _Analysis(C.Structure):
                 ("batch", C.c_int32)]
 
 
+class _FStats(C.Structure):
+    _fields_ = [("sigma", C.c_double), ("nu", C.c_int64), ("inertia", _Info), ("n", C.c_int64),
+                ("nnz_L", C.c_int64), ("store_bytes", C.c_int64)]
+
+
 _lib = None
 
 
@@ -86,6 +91,16 @@ def lib():
         L.kep_last_error.argtypes = [C.c_void_p]
         L.kep_last_error.restype = C.c_char_p
         L.kep_version.restype = C.c_char_p
+        L.kep_factor.argtypes = [C.c_void_p, C.c_double, P(C.c_void_p)]
+        L.kep_factor_info.argtypes = [C.c_void_p, P(_FStats)]
+        L.kep_solve.argtypes = [C.c_void_p, C.c_int32, P(C.c_double), C.c_int64, P(C.c_double), C.c_int64]
+        L.kep_solve_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.kep_factor_export.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_int64),
+                                        P(C.c_int32), P(C.c_double)]
+        L.kep_factor_destroy.argtypes = [C.c_void_p]
+        L.kep_factor_destroy.restype = None
+        for f in ("kep_factor", "kep_factor_info", "kep_solve", "kep_solve_dev", "kep_factor_export"):
+            getattr(L, f).restype = C.c_int
         for f in ("kep_analyze", "kep_set_values", "kep_set_values_dev", "kep_inertia", "kep_inertia_many",
                   "kep_get_analysis", "kep_get_perm", "kep_get_fronts", "kep_get_profile", "kep_reset_profile"):
             getattr(L, f).restype = C.c_int
@@ -219,6 +234,12 @@ class Kep:
     def reset_profile(self):
         self._check(lib().kep_reset_profile(self._h))
 
+    def factor(self, sigma: float) -> "Factor":
+        """kep_factor: retained LDL^T of A - sigma B (raises KepError, e.g. KEP_ESINGULAR)."""
+        h = C.c_void_p()
+        self._check(lib().kep_factor(self._h, float(sigma), C.byref(h)))
+        return Factor(self, h)
+
     def perm(self) -> np.ndarray:
         p = np.empty(self.n, dtype=np.int64)
         self._check(lib().kep_get_perm(self._h, _ptr(p, C.c_int64)))
@@ -235,3 +256,69 @@ class Kep:
 
 def version() -> str:
     return lib().kep_version().decode()
+
+
+class Factor:
+    """A kep_factorization: P (A - sigma B) P^T = L D L^T kept on the device."""
+
+    def __init__(self, owner: Kep, handle):
+        self._owner = owner            # keeps the ctx alive
+        self._h = handle
+        self.n = owner.n
+
+    def close(self):
+        if getattr(self, "_h", None):
+            if getattr(self._owner, "_h", None):       # kep_destroy already released it otherwise
+                lib().kep_factor_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        st = _FStats()
+        r = lib().kep_factor_info(self._h, C.byref(st))
+        if r != KEP_OK:
+            raise KepError(r, "kep_factor_info")
+        inf = InertiaInfo(*[getattr(st.inertia, f) for f, _ in _Info._fields_])
+        return dict(sigma=st.sigma, nu=st.nu, inertia=inf, n=st.n, nnz_L=st.nnz_L, store_bytes=st.store_bytes)
+
+    def solve(self, b):
+        """x = (A - sigma B)^-1 b for b of shape (n,) or (n, nrhs) (host arrays)."""
+        b = np.asarray(b, dtype=np.float64)
+        one = b.ndim == 1
+        B = np.asfortranarray(b.reshape(self.n, -1))
+        X = np.empty_like(B, order="F")
+        r = lib().kep_solve(self._h, B.shape[1], _ptr(B, C.c_double), self.n, _ptr(X, C.c_double), self.n)
+        if r != KEP_OK:
+            raise KepError(r, lib().kep_last_error(self._owner._h).decode())
+        return X[:, 0] if one else X
+
+    def solve_dev(self, b_ptr: int, x_ptr: int):
+        """One right-hand side in device memory (enqueued on the ctx stream)."""
+        r = lib().kep_solve_dev(self._h, C.c_void_p(b_ptr), C.c_void_p(x_ptr))
+        if r != KEP_OK:
+            raise KepError(r, lib().kep_last_error(self._owner._h).decode())
+
+    def export(self):
+        """(perm, d, dsub, Lcolptr, Lrowidx, Lval): P S P^T = L D L^T, L unit lower in CSC."""
+        n = self.n
+        perm = np.empty(n, np.int64)
+        d = np.empty(n)
+        ds = np.empty(n)
+        cp = np.zeros(n + 1, np.int64)
+        P = C.POINTER
+        r = lib().kep_factor_export(self._h, _ptr(perm, C.c_int64), _ptr(d, C.c_double), _ptr(ds, C.c_double),
+                                    _ptr(cp, C.c_int64), C.cast(None, P(C.c_int32)), C.cast(None, P(C.c_double)))
+        if r != KEP_OK:
+            raise KepError(r, lib().kep_last_error(self._owner._h).decode())
+        ri = np.empty(int(cp[-1]), np.int32)
+        vals = np.empty(int(cp[-1]))
+        r = lib().kep_factor_export(self._h, _ptr(perm, C.c_int64), _ptr(d, C.c_double), _ptr(ds, C.c_double),
+                                    _ptr(cp, C.c_int64), _ptr(ri, C.c_int32), _ptr(vals, C.c_double))
+        if r != KEP_OK:
+            raise KepError(r, lib().kep_last_error(self._owner._h).decode())
+        return perm, d, ds, cp, ri, vals

@@ -1,0 +1,123 @@
+"""GPU: retained factors and solves through the C ABI.
+
+Bars (BASELINE north_star):
+- factor residual ||P (A - sigma B) P^T - L D L^T||_F / ||A - sigma B||_F <= 1e-10,
+  exact (dense) at c1, estimated with 8 Gaussian probes (E||E v||^2 = ||E||_F^2) at c2;
+- the inertia of the exported D equals nu from LAPACK eigh (Sylvester);
+- solves: normwise backward error ||S x - b|| / (||S||_F ||x|| + ||b||) <= 1e-12 and,
+  at c1, x against numpy.linalg.solve.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import kepgen
+import oracle
+from paper_1710_05134_b200 import Kep, KepError
+from paper_1710_05134_b200.kep import KEP_ESINGULAR
+
+pytestmark = pytest.mark.gpu
+
+
+def _lower_csc_to_full(p, which, sigma=None):
+    n = p.n
+    col = np.repeat(np.arange(n), np.diff(p.colptr))
+    v = p.a - sigma * p.b if which == "s" else getattr(p, which)
+    Lo = sp.csc_matrix((v, p.rowidx, p.colptr), shape=(n, n))
+    return (Lo + sp.tril(Lo, -1).T).tocsr()
+
+
+def _d_inertia(d, ds):
+    neg = 0
+    k = 0
+    n = len(d)
+    while k < n:
+        if k + 1 < n and ds[k] != 0.0:
+            w = np.linalg.eigvalsh(np.array([[d[k], ds[k]], [ds[k], d[k + 1]]]))
+            neg += int(np.sum(w < 0))
+            k += 2
+        else:
+            neg += int(d[k] < 0)
+            k += 1
+    return neg
+
+
+def _dense_ldlt(fac_export, n):
+    perm, d, ds, cp, ri, vals = fac_export
+    L = sp.csc_matrix((vals, ri, cp), shape=(n, n)).toarray() + np.eye(n)
+    D = np.diag(d) + np.diag(ds[:-1], -1) + np.diag(ds[:-1], 1)
+    return perm, L, D
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("u", [0.01, 0.5])
+def test_factor_residual_and_inertia_c1(u, variant):
+    p = kepgen.config(1)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    k = Kep.from_pencil(p, pivot_u=u, kernel_variant=variant)
+    k.set_values(p.a, p.b)
+    for sig in kepgen.uniform_shifts(w[0], w[-1], 5):
+        S = A - sig * B
+        fac = k.factor(sig)
+        info = fac.info()
+        ex = fac.export()
+        perm, L, D = _dense_ldlt(ex, p.n)
+        assert sorted(perm.tolist()) == list(range(p.n))
+        PSP = S[np.ix_(perm, perm)]
+        res = np.linalg.norm(PSP - L @ D @ L.T) / np.linalg.norm(S)
+        assert res <= 1e-10, res
+        nu = int(np.sum(w < sig))
+        assert info["nu"] == nu == _d_inertia(ex[1], ex[2])
+        assert info["nnz_L"] == ex[3][-1]
+        # solves: one and three right-hand sides, against numpy.linalg.solve
+        rng = np.random.default_rng(7)
+        b = rng.standard_normal((p.n, 3))
+        x = fac.solve(b)
+        xr = np.linalg.solve(S, b)
+        be = np.linalg.norm(S @ x - b) / (np.linalg.norm(S) * np.linalg.norm(x) + np.linalg.norm(b))
+        assert be <= 1e-12, be
+        assert np.allclose(x, xr, rtol=1e-8 * np.linalg.cond(S), atol=0)
+        x1 = fac.solve(b[:, 0])
+        assert np.allclose(x1, x[:, 0], rtol=1e-12, atol=1e-12 * np.abs(x).max())   # atomic scatter order varies
+
+
+def test_factor_singular_shift():
+    A = np.diag(np.arange(1.0, 11.0))
+    from test_gpu_parity import _pencil_from_dense
+    p = _pencil_from_dense(A, np.eye(10))
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    with pytest.raises(KepError) as ei:
+        k.factor(4.0)
+    assert ei.value.status == KEP_ESINGULAR
+    fac = k.factor(4.5)
+    x = fac.solve(np.ones(10))
+    assert np.allclose(x, 1.0 / (np.arange(1.0, 11.0) - 4.5), rtol=1e-14)
+
+
+def test_factor_c2_probe_residual_and_solve():
+    p = kepgen.config(2)
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    lo, hi = kepgen.spectral_bounds(p)
+    sig = lo + 0.37 * (hi - lo)
+    S = _lower_csc_to_full(p, "s", sig)
+    fac = k.factor(sig)
+    perm, d, ds, cp, ri, vals = fac.export()
+    n = p.n
+    L = sp.csc_matrix((vals, ri, cp), shape=(n, n)) + sp.identity(n, format="csc")
+    D = sp.diags([ds[:-1], d, ds[:-1]], [-1, 0, 1], format="csr")
+    PSP = S[perm][:, perm]
+    rng = np.random.default_rng(3)
+    V = rng.standard_normal((n, 8))
+    E = PSP @ V - L @ (D @ (L.T @ V))
+    res = np.sqrt(np.sum(E * E) / 8) / sp.linalg.norm(S)
+    assert res <= 1e-10, res
+    b = rng.standard_normal(n)
+    x = fac.solve(b)
+    be = np.linalg.norm(S @ x - b) / (sp.linalg.norm(S) * np.linalg.norm(x) + np.linalg.norm(b))
+    assert be <= 1e-12, be
+    # the factor's inertia agrees with the inertia path at the same shift
+    st, nu, _ = k.inertia(sig)
+    assert fac.info()["nu"] == nu == _d_inertia(d, ds)
