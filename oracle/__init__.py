@@ -32,6 +32,9 @@ Modules
                   tridiagonal Sturm counts (P5).
 - ``symbolic``    brute-force boolean elimination (nnz of L, etree) for the
                   symbolic pins.
+- ``lanczos``     stage 1 (Alg. 2, generalized Lanczos Eq. 2.1) and stage 3
+                  (Alg. 3, SI Lanczos Eq. 2.4 with error bounds Eq. 3.1 and
+                  tests 3.3-3.5), step by step.
 
 Pins (what each is checked against, in ``tests/test_oracle_*.py``) are listed
 in DESIGN.md §"Oracle and pins".  Parity unpinned: L, D, pivot order, delayed
@@ -41,9 +44,11 @@ from .eig import nu_eig, eigvals_pencil
 from .dense_bk import ALPHA, bk_ldl, nu_dense, block_inertia_2x2, Inertia, reconstruct
 from .closed_form import twin_eigenvalues, nu_twin, sturm_count
 from .sparse_mf import nu_sparse, SparseOracle
+from .lanczos import lanczos_decomposition, initial_interval_alg2, si_lanczos_alg3, tridiag_eig
 
 __all__ = [
     "nu_eig", "eigvals_pencil", "ALPHA", "bk_ldl", "nu_dense", "block_inertia_2x2",
     "Inertia", "reconstruct", "twin_eigenvalues", "nu_twin", "sturm_count",
-    "nu_sparse", "SparseOracle",
+    "nu_sparse", "SparseOracle", "lanczos_decomposition", "initial_interval_alg2", "si_lanczos_alg3",
+    "tridiag_eig",
 ]
