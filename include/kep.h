@@ -196,6 +196,10 @@ typedef struct {
  * is returned), KEP_ENOMEM, KEP_ECUDA, KEP_EINVAL (values not set). */
 KEP_API kep_status kep_factor(kep_ctx* ctx, double sigma, kep_factorization** out);
 
+/* Same for alpha A - sigma B (e.g. alpha = 0, sigma = -1 factorises B for the
+ * B-solves of stage 1's generalized Lanczos). */
+KEP_API kep_status kep_factor_pencil(kep_ctx* ctx, double alpha, double sigma, kep_factorization** out);
+
 /* Factor statistics (shift, nu, inertia, size of L). */
 KEP_API kep_status kep_factor_info(const kep_factorization* f, kep_factor_stats* out);
 
@@ -218,6 +222,51 @@ KEP_API kep_status kep_factor_export(const kep_factorization* f, int64_t* perm, 
 
 /* Release a factor.  kep_destroy(ctx) releases the factors still alive on ctx. */
 KEP_API void kep_factor_destroy(kep_factorization* f);
+
+/* ---------------------------------------------------------------------------
+ * The three-stage k-th eigenpair method (Alg. 4; SURVEY.md
+ * §8(f) rows f2, f3).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int32_t m_max;              /* stage 2 stops when nu_u - nu_l <= m_max (default 20); <= 32 */
+    double tau_res;             /* relative residual 2-norm tolerance, test (3.3)-(3.5) line (default 1e-10) */
+    double tau_diff;            /* relative difference 2-norm tolerance, Eq. (3.5) (default 1e-10) */
+    int32_t max_lanczos;        /* stage-1 Lanczos steps cap (default 64) */
+    int32_t max_bisect;         /* stage-2 rounds cap (default 128) */
+    int32_t max_si;             /* stage-3 SI Lanczos steps cap (default 500) */
+    int32_t shifts_per_round;   /* stage-2 multisection width P (1 = Alg. 1', default 1) */
+    uint64_t seed;              /* seed of the start vectors (splitmix64, uniform(-1,1)) when v0s are NULL */
+    const double* v0_stage1;    /* optional start vector of stage 1 (n, host) */
+    const double* v0_stage3;    /* optional start vector of stage 3 (n, host) */
+} kep_kth_opts;
+
+typedef struct {
+    double s1_lower, s1_upper;          /* stage-1 interval [sigma_l, sigma_u) (Alg. 2) */
+    int64_t s1_nu_lower, s1_nu_upper;
+    double sigma_lower, sigma_upper;    /* stage-2 interval, nu_u - nu_l <= m_max */
+    int64_t nu_lower, nu_upper;
+    double sigma_si;                    /* stage-3 shift (interval midpoint) */
+    int32_t stage1_iters, stage2_rounds, stage2_shifts, stage3_iters;
+    double eta;                         /* error bound Eq. (3.1) of lambda_k */
+    double rel_residual;                /* ||(A - lambda B) x||_2 / ||x||_2 */
+    double rel_diff;                    /* Eq. (3.5) at the last step */
+    double seconds[3];                  /* wall time per stage */
+    kep_status status;                  /* KEP_OK, KEP_ECLUSTER (cluster suspected), KEP_ENOCONV */
+} kep_kth_report;
+
+KEP_API void kep_default_kth_opts(kep_kth_opts* o);
+
+/* lambda_k (1-based k, k-th smallest) and optionally its eigenvector x (n,
+ * host; B-normalised) of A x = lambda B x with the index validated: stage 1
+ * (Alg. 2) brackets lambda_k with Ritz values, stage 2 (Alg. 1') narrows the
+ * bracket with nu_sigma until it holds <= m_max eigenvalues, stage 3 (Alg. 3)
+ * runs SI Lanczos at its midpoint until the m error bounds (3.1) are inside the
+ * interval and disjoint and every pair meets tau_res and tau_diff; lambda_k is
+ * the (k - nu_l)-th of them.  Returns KEP_OK (report->status may be
+ * KEP_ECLUSTER or KEP_ENOCONV: lambda not written), or an error.  report may
+ * be NULL. */
+KEP_API kep_status kep_kth_eigenpair(kep_ctx* ctx, int64_t k, const kep_kth_opts* opts, double* lambda, double* x,
+                                     kep_kth_report* report);
 
 /* Analysis statistics (sizes, #nzf, flops per shift, memory). */
 KEP_API kep_status kep_get_analysis(const kep_ctx* ctx, kep_analysis_info* info);

@@ -5,6 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <ctime>
+#include <numeric>
 #include <cstdio>
 #include <cstdlib>
 #include <cfloat>
@@ -36,6 +40,11 @@ struct kep_ctx {
     int32_t *d_child_ptr = nullptr, *d_child_list = nullptr, *d_level_fronts = nullptr;
     int32_t *d_piv_first = nullptr, *d_cb_ptr = nullptr, *d_cb_rows = nullptr;
     int64_t *d_perm = nullptr, *d_iperm = nullptr;          // elimination position <-> dof
+    // full symmetric CSR of the union pattern (stage-1/3 SpMV): 20 B per stored nonzero
+    int64_t *d_csr_rp = nullptr, *d_csr_src = nullptr;
+    int32_t* d_csr_ci = nullptr;
+    double *d_csr_a = nullptr, *d_csr_b = nullptr;
+    int64_t csr_nnz = 0;
     int64_t *d_arena_off = nullptr, *d_asm_ptr = nullptr, *d_asm_src = nullptr, *d_rmap_ptr = nullptr;
     uint32_t* d_asm_rc = nullptr;
     int32_t* d_rmap = nullptr;
@@ -46,6 +55,7 @@ struct kep_ctx {
     int32_t *d_nd_in = nullptr, *d_nd_out = nullptr, *d_doff = nullptr;
     ShiftStat* d_stats = nullptr;
     double* d_sigma = nullptr;
+    double* d_alpha = nullptr;
     std::vector<ShiftStat> h_stats;
     // per-level launch lists: fast (panel + Schur) and reference fronts
     int32_t* d_lists = nullptr;                 // [fast fronts of all levels | ref fronts of all levels]
@@ -74,7 +84,7 @@ struct kep_ctx {
 // Retained factors of one shift.
 struct kep_factorization {
     kep_ctx* ctx = nullptr;
-    double sigma = 0.0;
+    double sigma = 0.0, alpha = 1.0;
     int64_t nu = 0;
     kep_inertia_info info{};
     // store (device) + offsets and level structure captured at creation
@@ -131,6 +141,7 @@ void free_batch(kep_ctx* c) {
     cudaFree(c->d_doff); c->d_doff = nullptr;
     cudaFree(c->d_stats); c->d_stats = nullptr;
     cudaFree(c->d_sigma); c->d_sigma = nullptr;
+    cudaFree(c->d_alpha); c->d_alpha = nullptr;
     cudaFree(c->d_aux); c->d_aux = nullptr;
     cudaFree(c->d_flag); c->d_flag = nullptr;
     cudaFree(c->d_forced); c->d_forced = nullptr;
@@ -157,6 +168,7 @@ kep_status alloc_batch(kep_ctx* c) {
     KEP_CUDA(c, cudaMalloc(&c->d_doff, nfb));
     KEP_CUDA(c, cudaMalloc(&c->d_stats, sizeof(ShiftStat) * cap));
     KEP_CUDA(c, cudaMalloc(&c->d_sigma, sizeof(double) * cap));
+    KEP_CUDA(c, cudaMalloc(&c->d_alpha, sizeof(double) * cap));
     KEP_CUDA(c, cudaMalloc(&c->d_aux, sizeof(double) * std::max<int64_t>(c->aux_stride, 1) * cap));
     KEP_CUDA(c, cudaMalloc(&c->d_flag, nfb));
     KEP_CUDA(c, cudaMemset(c->d_flag, 0, nfb));
@@ -240,8 +252,41 @@ kep_status build_lists(kep_ctx* c) {
     return KEP_OK;
 }
 
-kep_status upload_plan(kep_ctx* c) {
+// full symmetric CSR (both triangles) of the lower CSC pattern; src = lower entry index
+void build_full_csr(int64_t n, const int64_t* colptr, const int32_t* rowidx, std::vector<int64_t>& rp,
+                    std::vector<int32_t>& ci, std::vector<int64_t>& src) {
+    rp.assign(n + 1, 0);
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t q = colptr[j]; q < colptr[j + 1]; ++q) {
+            const int64_t i = rowidx[q];
+            rp[i + 1]++;
+            if (i != j) rp[j + 1]++;
+        }
+    for (int64_t i = 0; i < n; ++i) rp[i + 1] += rp[i];
+    ci.assign(rp[n], 0);
+    src.assign(rp[n], 0);
+    std::vector<int64_t> w(rp.begin(), rp.end() - 1);
+    for (int64_t j = 0; j < n; ++j)                  // rows get their columns in increasing order
+        for (int64_t q = colptr[j]; q < colptr[j + 1]; ++q) {
+            const int64_t i = rowidx[q];
+            ci[w[i]] = (int32_t)j; src[w[i]++] = q;
+            if (i != j) { ci[w[j]] = (int32_t)i; src[w[j]++] = q; }
+        }
+}
+
+kep_status upload_plan(kep_ctx* c, const int64_t* colptr, const int32_t* rowidx) {
     const Symbolic& S = c->sym;
+    {
+        std::vector<int64_t> rp, src;
+        std::vector<int32_t> ci;
+        build_full_csr(S.n, colptr, rowidx, rp, ci, src);
+        c->csr_nnz = rp[S.n];
+        KEP_CUDA(c, upload(&c->d_csr_rp, rp));
+        KEP_CUDA(c, upload(&c->d_csr_ci, ci));
+        KEP_CUDA(c, upload(&c->d_csr_src, src));
+        KEP_CUDA(c, cudaMalloc(&c->d_csr_a, std::max<int64_t>(c->csr_nnz, 1) * sizeof(double)));
+        KEP_CUDA(c, cudaMalloc(&c->d_csr_b, std::max<int64_t>(c->csr_nnz, 1) * sizeof(double)));
+    }
     KEP_CUDA(c, upload(&c->d_forder, S.forder));
     KEP_CUDA(c, upload(&c->d_npiv, S.npiv));
     KEP_CUDA(c, upload(&c->d_ncb, S.ncb));
@@ -313,6 +358,7 @@ DevPlan make_plan(kep_ctx* c) {
     P.doff = c->d_doff;
     P.stats = c->d_stats;
     P.sigma = c->d_sigma;
+    P.alpha = c->d_alpha;
     P.u = c->opts.pivot_u;
     P.aux = c->d_aux;
     P.aux_stride = c->aux_stride;
@@ -363,7 +409,8 @@ kep_status prepare_store(kep_ctx* c, kep_factorization* k) {
 
 // One batch of `m` shifts through every level.  Fills c->h_stats[0..m).
 // keep != NULL (m == 1): the factors are copied into keep's store level by level.
-kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization* keep = nullptr) {
+kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization* keep = nullptr,
+                     double alpha = 1.0) {
     for (int attempt = 0; attempt < 8; ++attempt) {
         if (m > c->batch_cap) return fail(c, KEP_EINVAL, "internal: batch larger than capacity");
         if (keep) {
@@ -371,6 +418,11 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             if (r != KEP_OK) return r;
         }
         KEP_CUDA(c, cudaMemcpyAsync(c->d_sigma, sigmas, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+        {
+            std::vector<double> al(m, alpha);
+            KEP_CUDA(c, cudaMemcpyAsync(c->d_alpha, al.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+            KEP_CUDA(c, cudaStreamSynchronize(c->stream));      // al is a local buffer
+        }
         kep::launch_reset_stats(c->d_stats, m, c->stream);
         c->prof.other_launches += 1;
         if (const char* fill = getenv("KEP_DEBUG_FILL"))       // debug: poison the front arena
@@ -574,7 +626,7 @@ kep_status kep_analyze(int64_t n, const int64_t* colptr, const int32_t* rowidx, 
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { delete c; return fail(nullptr, KEP_ECUDA, "stream creation failed"); }
         c->own_stream = true;
     }
-    kep_status st = upload_plan(c);
+    kep_status st = upload_plan(c, colptr, rowidx);
     if (st != KEP_OK) { std::string m = c->err; kep_destroy(c); return fail(nullptr, st, m); }
     *out = c;
     return KEP_OK;
@@ -586,6 +638,8 @@ kep_status kep_set_values_dev(kep_ctx* c, const double* a_dev, const double* b_d
     KEP_CUDA(c, cudaSetDevice(c->device));
     kep::launch_gather(a_dev, c->d_asm_src, c->d_a, c->sym.nnz, c->stream);
     kep::launch_gather(b_dev, c->d_asm_src, c->d_b, c->sym.nnz, c->stream);
+    kep::launch_gather(a_dev, c->d_csr_src, c->d_csr_a, c->csr_nnz, c->stream);
+    kep::launch_gather(b_dev, c->d_csr_src, c->d_csr_b, c->csr_nnz, c->stream);
     KEP_CUDA(c, cudaGetLastError());
     KEP_CUDA(c, cudaStreamSynchronize(c->stream));
     c->values_set = true;
@@ -663,6 +717,10 @@ kep_status kep_inertia(kep_ctx* c, double sigma, int64_t* nu, kep_inertia_info* 
 }
 
 kep_status kep_factor(kep_ctx* c, double sigma, kep_factorization** out) {
+    return kep_factor_pencil(c, 1.0, sigma, out);
+}
+
+kep_status kep_factor_pencil(kep_ctx* c, double alpha, double sigma, kep_factorization** out) {
     if (!c || !out) return fail(c, KEP_EINVAL, "null argument");
     *out = nullptr;
     if (!c->have_device) return fail(c, KEP_ENODEVICE, "no CUDA device");
@@ -672,7 +730,8 @@ kep_status kep_factor(kep_ctx* c, double sigma, kep_factorization** out) {
     if (!k) return fail(c, KEP_ENOMEM, "host allocation failed");
     k->ctx = c;
     k->sigma = sigma;
-    kep_status st = run_batch(c, 1, &sigma, k);
+    k->alpha = alpha;
+    kep_status st = run_batch(c, 1, &sigma, k, alpha);
     if (st != KEP_OK) { kep_factor_destroy(k); return st; }
     const ShiftStat& S = c->h_stats[0];
     const double minpiv = bits_to_double(S.minpiv_bits), smax = bits_to_double(S.smax_bits);
@@ -830,6 +889,322 @@ void kep_factor_destroy(kep_factorization* k) {
     delete k;
 }
 
+void kep_default_kth_opts(kep_kth_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->m_max = 20;
+    o->tau_res = 1e-10;
+    o->tau_diff = 1e-10;
+    o->max_lanczos = 64;
+    o->max_bisect = 128;
+    o->max_si = 500;
+    o->shifts_per_round = 1;
+    o->seed = 1;
+}
+
+namespace {
+
+// splitmix64 -> uniform(-1, 1)
+void seeded_uniform(uint64_t seed, int64_t n, std::vector<double>& v) {
+    v.resize(n);
+    uint64_t x = seed;
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        v[i] = 2.0 * ((double)(z >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
+    }
+}
+
+struct DevVec {
+    double* p = nullptr;
+    ~DevVec() { cudaFree(p); }
+};
+
+// Lanczos helpers on the ctx stream (dot products come back to the host)
+struct Lz {
+    kep_ctx* c;
+    double* dtmp = nullptr;          // device scratch for reductions (>= 512 doubles)
+    double dot(const double* x, const double* y) {
+        kep::launch_gemv_t(x, 0, 1, y, c->sym.n, dtmp, c->stream);
+        double v = 0.0;
+        cudaMemcpyAsync(&v, dtmp, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+        cudaStreamSynchronize(c->stream);
+        return v;
+    }
+    void spmv(const double* x, double* ya, double* yb) {
+        kep::launch_spmv2(c->d_csr_rp, c->d_csr_ci, c->d_csr_a, c->d_csr_b, x, ya, yb, c->sym.n, c->stream);
+    }
+    // r -= U (V^T r), twice (full reorthogonalisation in the B-inner product)
+    void reorth(const double* V, const double* U, int j, double* r) {
+        for (int pass = 0; pass < 2; ++pass) {
+            kep::launch_gemv_t(V, c->sym.n, j, r, c->sym.n, dtmp, c->stream);
+            kep::launch_combine(U, c->sym.n, j, dtmp, -1.0, 1.0, r, 0.0, nullptr, 0.0, nullptr, c->sym.n, c->stream);
+        }
+    }
+};
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+kep_status kep_kth_eigenpair(kep_ctx* c, int64_t k, const kep_kth_opts* opts_in, double* lambda, double* x,
+                             kep_kth_report* rep_out) {
+    if (!c || !lambda) return fail(c, KEP_EINVAL, "null argument");
+    if (!c->have_device) return fail(c, KEP_ENODEVICE, "no CUDA device");
+    if (!c->values_set) return fail(c, KEP_EINVAL, "kep_set_values must precede kep_kth_eigenpair");
+    const int64_t n = c->sym.n;
+    if (k < 1 || k > n) return fail(c, KEP_EINVAL, "k out of range");
+    kep_kth_opts o;
+    if (opts_in) o = *opts_in; else kep_default_kth_opts(&o);
+    if (o.m_max < 1 || o.m_max > 32) return fail(c, KEP_EINVAL, "m_max must be in [1, 32]");
+    if (o.shifts_per_round < 1) o.shifts_per_round = 1;
+    KEP_CUDA(c, cudaSetDevice(c->device));
+    kep_kth_report R;
+    std::memset(&R, 0, sizeof(R));
+    R.status = KEP_OK;
+    Lz L{c};
+    DevVec tmp;
+    KEP_CUDA(c, cudaMalloc(&tmp.p, sizeof(double) * 1024));
+    L.dtmp = tmp.p;
+    auto nu_at = [&](double& sig, int64_t& nu) -> kep_status {     // nu_sigma, perturbing an exact hit
+        for (int t = 0; t < 8; ++t) {
+            kep_status st = kep_inertia(c, sig, &nu, nullptr);
+            if (st == KEP_OK) return KEP_OK;
+            if (st != KEP_ESINGULAR) return st;
+            sig += (std::fabs(sig) + 1e-300) * 1e-12 * (1 << t);
+        }
+        return fail(c, KEP_ESINGULAR, "shift stays singular after perturbation");
+    };
+    // ------------------------------------------------------------ stage 1 (Alg. 2)
+    double t0 = now_s();
+    const int J1 = std::max(2, o.max_lanczos);
+    DevVec V, U, w, r, yb;
+    KEP_CUDA(c, cudaMalloc(&V.p, sizeof(double) * n * (J1 + 1)));
+    KEP_CUDA(c, cudaMalloc(&U.p, sizeof(double) * n * (J1 + 1)));
+    KEP_CUDA(c, cudaMalloc(&w.p, sizeof(double) * n));
+    KEP_CUDA(c, cudaMalloc(&r.p, sizeof(double) * n));
+    KEP_CUDA(c, cudaMalloc(&yb.p, sizeof(double) * n));
+    std::vector<double> h0;
+    if (o.v0_stage1) h0.assign(o.v0_stage1, o.v0_stage1 + n); else seeded_uniform(o.seed, n, h0);
+    KEP_CUDA(c, cudaMemcpyAsync(V.p, h0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    L.spmv(V.p, nullptr, yb.p);
+    double nb = std::sqrt(L.dot(V.p, yb.p));
+    kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 1.0 / nb, V.p, 0.0, nullptr, 0.0, nullptr, n, c->stream);
+    kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 0.0, U.p, 1.0 / nb, yb.p, 0.0, nullptr, n, c->stream);
+    kep_factorization* FB = nullptr;
+    {
+        kep_status st = kep_factor_pencil(c, 0.0, -1.0, &FB);            // B = 0 A - (-1) B
+        if (st == KEP_ESINGULAR) return fail(c, KEP_ENOTSPD, "B is singular");
+        if (st != KEP_OK) return st;
+    }
+    if (FB->info.n_neg != 0 || FB->info.n_zero != 0) {
+        kep_factor_destroy(FB);
+        return fail(c, KEP_ENOTSPD, "B is not positive definite (S:448)");
+    }
+    std::vector<double> al, be;
+    double sig_prev = 0.0, sig = 0.0;
+    int64_t nu_prev = 0, nu = 0;
+    bool bracketed = false;
+    for (int j = 1; j <= J1; ++j) {
+        double* vj = V.p + (size_t)(j - 1) * n;
+        double* uj = U.p + (size_t)(j - 1) * n;
+        L.spmv(vj, w.p, nullptr);                                           // A v_j
+        const double a = L.dot(vj, w.p);
+        kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 1.0, w.p, -a, uj, j > 1 ? -be.back() : 0.0,
+                            j > 1 ? uj - n : nullptr, n, c->stream);
+        L.reorth(V.p, U.p, j, w.p);                                         // rh
+        kep_status st = kep_solve_dev(FB, w.p, r.p);                         // r = B^-1 rh
+        if (st != KEP_OK) { kep_factor_destroy(FB); return st; }
+        const double b = std::sqrt(std::max(L.dot(w.p, r.p), 0.0));
+        al.push_back(a);
+        be.push_back(b);
+        std::vector<double> d(al), Z;
+        kep::tridiag_eigen(d, std::vector<double>(be.begin(), be.end() - 1), Z);   // Eq. (2.2)
+        sig = (k <= nu_prev) ? d.front() : d.back();
+        st = nu_at(sig, nu);
+        if (st != KEP_OK) { kep_factor_destroy(FB); return st; }
+        R.stage1_iters = j;
+        if (j != 1 && ((nu < k && k <= nu_prev) || (nu_prev < k && k <= nu))) { bracketed = true; break; }
+        sig_prev = sig;
+        nu_prev = nu;
+        if (b == 0.0) break;                                                 // invariant subspace
+        kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 0.0, vj + n, 1.0 / b, r.p, 0.0, nullptr, n, c->stream);
+        kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 0.0, uj + n, 1.0 / b, w.p, 0.0, nullptr, n, c->stream);
+    }
+    kep_factor_destroy(FB);
+    if (!bracketed) return fail(c, KEP_ENOCONV, "stage 1 (Alg. 2) did not bracket lambda_k");
+    double lo = std::min(sig_prev, sig), hi = std::max(sig_prev, sig);
+    int64_t nlo = std::min(nu_prev, nu), nhi = std::max(nu_prev, nu);
+    R.s1_lower = lo; R.s1_upper = hi; R.s1_nu_lower = nlo; R.s1_nu_upper = nhi;
+    R.seconds[0] = now_s() - t0;
+    // ------------------------------------------------------------ stage 2 (Alg. 1', P shifts per round)
+    t0 = now_s();
+    const int P = o.shifts_per_round;
+    std::vector<double> sg(P);
+    std::vector<int64_t> nv(P);
+    std::vector<kep_status> ps(P);
+    while (nhi - nlo > o.m_max) {
+        if (R.stage2_rounds >= o.max_bisect || hi - lo <= 4.0 * DBL_EPSILON * std::max(std::fabs(lo), std::fabs(hi))) {
+            R.status = KEP_ECLUSTER;
+            break;
+        }
+        for (int i = 0; i < P; ++i) sg[i] = lo + (hi - lo) * (double)(i + 1) / (double)(P + 1);
+        kep_status st = kep_inertia_many(c, P, sg.data(), nv.data(), ps.data(), nullptr);
+        if (st != KEP_OK) return st;
+        for (int i = 0; i < P; ++i)
+            if (ps[i] != KEP_OK) {                                           // perturb toward the wider side
+                sg[i] += 1e-6 * (hi - lo);
+                st = nu_at(sg[i], nv[i]);
+                if (st != KEP_OK) return st;
+            }
+        R.stage2_rounds++;
+        R.stage2_shifts += P;
+        double l2 = lo, h2 = hi;
+        int64_t nl2 = nlo, nh2 = nhi;
+        for (int i = 0; i <= P; ++i) {                                       // first pair with nu_a < k <= nu_b
+            const double sa = i == 0 ? lo : sg[i - 1], sb = i == P ? hi : sg[i];
+            const int64_t na = i == 0 ? nlo : nv[i - 1], nbb = i == P ? nhi : nv[i];
+            if (na < k && k <= nbb) { l2 = sa; h2 = sb; nl2 = na; nh2 = nbb; break; }
+        }
+        lo = l2; hi = h2; nlo = nl2; nhi = nh2;
+    }
+    R.sigma_lower = lo; R.sigma_upper = hi; R.nu_lower = nlo; R.nu_upper = nhi;
+    R.seconds[1] = now_s() - t0;
+    if (R.status != KEP_OK) {
+        if (rep_out) *rep_out = R;
+        return KEP_OK;
+    }
+    // ------------------------------------------------------------ stage 3 (Alg. 3)
+    t0 = now_s();
+    const int64_t l = k - nlo, m = nhi - nlo;
+    double sigma = 0.5 * (lo + hi);
+    kep_factorization* F = nullptr;
+    for (int t = 0; t < 8; ++t) {
+        kep_status st = kep_factor(c, sigma, &F);
+        if (st == KEP_OK) break;
+        if (st != KEP_ESINGULAR) return st;
+        sigma += 1e-6 * (hi - lo);
+    }
+    if (!F) return fail(c, KEP_ESINGULAR, "stage-3 shift stays singular");
+    R.sigma_si = sigma;
+    const int J3 = std::max<int>(o.max_si, (int)m);
+    DevVec W, Vt, X, Xp, g, Cm, ta, tb;
+    KEP_CUDA(c, cudaMalloc(&ta.p, sizeof(double) * n));                  // scratch of the convergence tests
+    KEP_CUDA(c, cudaMalloc(&tb.p, sizeof(double) * n));
+    KEP_CUDA(c, cudaMalloc(&W.p, sizeof(double) * n * (J3 + 1)));
+    KEP_CUDA(c, cudaMalloc(&Vt.p, sizeof(double) * n * (J3 + 1)));
+    KEP_CUDA(c, cudaMalloc(&X.p, sizeof(double) * n * m));
+    KEP_CUDA(c, cudaMalloc(&Xp.p, sizeof(double) * n * m));
+    KEP_CUDA(c, cudaMalloc(&g.p, sizeof(double) * 64));
+    KEP_CUDA(c, cudaMalloc(&Cm.p, sizeof(double) * (size_t)(J3 + 1) * m));
+    if (o.v0_stage3) h0.assign(o.v0_stage3, o.v0_stage3 + n); else seeded_uniform(o.seed + 0x5151, n, h0);
+    KEP_CUDA(c, cudaMemcpyAsync(W.p, h0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    L.spmv(W.p, nullptr, yb.p);
+    nb = std::sqrt(L.dot(W.p, yb.p));
+    kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 1.0 / nb, W.p, 0.0, nullptr, 0.0, nullptr, n, c->stream);
+    kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 0.0, Vt.p, 1.0 / nb, yb.p, 0.0, nullptr, n, c->stream);
+    al.clear();
+    be.clear();
+    bool have_prev = false, done = false;
+    double lam_k = 0.0;
+    int iq_k = -1;
+    std::vector<double> hres(m), hdif(m);
+    for (int j = 1; j <= J3 && !done; ++j) {
+        double* wj = W.p + (size_t)(j - 1) * n;
+        double* vj = Vt.p + (size_t)(j - 1) * n;
+        kep_status st = kep_solve_dev(F, vj, r.p);                           // z = (A - sigma B)^-1 v~_j
+        if (st != KEP_OK) { kep_factor_destroy(F); return st; }
+        const double a = L.dot(vj, r.p);
+        kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 1.0, r.p, -a, wj, j > 1 ? -be.back() : 0.0,
+                            j > 1 ? wj - n : nullptr, n, c->stream);
+        L.reorth(Vt.p, W.p, j, r.p);
+        L.spmv(r.p, nullptr, yb.p);                                          // u = B r
+        const double b = std::sqrt(std::max(L.dot(r.p, yb.p), 0.0));
+        al.push_back(a);
+        be.push_back(b);
+        R.stage3_iters = j;
+        if (j >= m) {
+            std::vector<double> th(al), Z;
+            kep::tridiag_eigen(th, std::vector<double>(be.begin(), be.end() - 1), Z);   // Eq. (2.5)
+            std::vector<int> ord(j);
+            std::iota(ord.begin(), ord.end(), 0);
+            std::stable_sort(ord.begin(), ord.end(), [&](int p1, int p2) { return std::fabs(th[p1]) > std::fabs(th[p2]); });
+            std::vector<double> lam(m), eta(m), Ch((size_t)j * m), gh(m);
+            for (int q = 0; q < m; ++q) {
+                const int i = ord[q];
+                const double yj = Z[(size_t)(j - 1) + (size_t)i * j];
+                lam[q] = sigma + 1.0 / th[i];                                  // Eq. (2.6)
+                const double rho = std::fabs(b * yj / th[i]);
+                eta[q] = rho / std::fabs(th[i]) / std::sqrt(1.0 + rho * rho); // Eq. (3.1)
+                for (int t = 0; t < j; ++t) Ch[t + (size_t)q * j] = th[i] * Z[t + (size_t)i * j];
+                gh[q] = yj;                                                  // x = theta W y + r (e_j^T y)
+            }
+            bool inc = true, dis = true;
+            for (int q = 0; q < m; ++q) inc = inc && lam[q] - eta[q] >= lo && lam[q] + eta[q] < hi;   // (3.3)
+            std::vector<int> so(m);
+            std::iota(so.begin(), so.end(), 0);
+            std::sort(so.begin(), so.end(), [&](int p1, int p2) { return lam[p1] < lam[p2]; });
+            for (int q = 0; q + 1 < m; ++q)                                                         // (3.4)
+                dis = dis && lam[so[q]] + eta[so[q]] < lam[so[q + 1]] - eta[so[q + 1]];
+            KEP_CUDA(c, cudaMemcpyAsync(Cm.p, Ch.data(), sizeof(double) * Ch.size(), cudaMemcpyHostToDevice, c->stream));
+            KEP_CUDA(c, cudaMemcpyAsync(g.p, gh.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+            kep::launch_ritz(W.p, n, j, Cm.p, r.p, g.p, (int)m, X.p, n, n, c->stream);   // x_{i,2}, Eq. (2.7)
+            bool conv = inc && dis && have_prev;
+            for (int q = 0; q < m; ++q) {
+                if (!conv) break;
+                double* xq = X.p + (size_t)q * n;
+                const double xx = L.dot(xq, xq);
+                L.spmv(xq, ta.p, tb.p);                                       // (A - lambda B) x
+                kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 1.0, ta.p, -lam[q], tb.p, 0.0, nullptr, n, c->stream);
+                hres[q] = std::sqrt(L.dot(ta.p, ta.p) / xx);
+                double* xpq = Xp.p + (size_t)q * n;
+                const double pp = L.dot(xpq, xpq), xp = L.dot(xq, xpq);
+                const double sc = (xp < 0 ? -1.0 : 1.0) * std::sqrt(pp / xx);      // equal 2-norms, aligned signs
+                kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 0.0, ta.p, sc, xq, -1.0, xpq, n, c->stream);
+                hdif[q] = std::sqrt(L.dot(ta.p, ta.p) / pp);                       // Eq. (3.5)
+                conv = conv && hres[q] < o.tau_res && hdif[q] < o.tau_diff;
+            }
+            KEP_CUDA(c, cudaMemcpyAsync(Xp.p, X.p, sizeof(double) * n * m, cudaMemcpyDeviceToDevice, c->stream));
+            have_prev = true;
+            if (conv) {
+                const int q = so[l - 1];                                       // back to increasing order
+                lam_k = lam[q];
+                iq_k = q;
+                R.eta = eta[q];
+                R.rel_residual = hres[q];
+                R.rel_diff = hdif[q];
+                done = true;
+                break;
+            }
+        }
+        if (b == 0.0) break;
+        kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 0.0, wj + n, 1.0 / b, r.p, 0.0, nullptr, n, c->stream);
+        kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 0.0, vj + n, 1.0 / b, yb.p, 0.0, nullptr, n, c->stream);
+    }
+    kep_factor_destroy(F);
+    R.seconds[2] = now_s() - t0;
+    if (!done) {
+        R.status = KEP_ENOCONV;
+        if (rep_out) *rep_out = R;
+        return KEP_OK;
+    }
+    *lambda = lam_k;
+    if (x) {                                                                   // B-normalised eigenvector
+        double* xq = X.p + (size_t)iq_k * n;
+        L.spmv(xq, nullptr, yb.p);
+        const double bn = std::sqrt(L.dot(xq, yb.p));
+        kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 1.0 / bn, xq, 0.0, nullptr, 0.0, nullptr, n, c->stream);
+        KEP_CUDA(c, cudaMemcpyAsync(x, xq, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        KEP_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    if (rep_out) *rep_out = R;
+    return KEP_OK;
+}
+
 kep_status kep_get_analysis(const kep_ctx* c, kep_analysis_info* I) {
     if (!c || !I) return KEP_EINVAL;
     const Symbolic& S = c->sym;
@@ -893,7 +1268,8 @@ void kep_destroy(kep_ctx* c) {
                         c->d_level_fronts, c->d_arena_off, c->d_asm_ptr, c->d_asm_src, c->d_rmap_ptr,
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
-                        c->d_cb_rows, c->d_perm, c->d_iperm};
+                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci,
+                        c->d_csr_a, c->d_csr_b};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

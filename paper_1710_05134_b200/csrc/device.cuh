@@ -44,6 +44,7 @@ struct DevPlan {
     int32_t* doff;               // [batch][nf] offset of a child's delayed block in its parent
     ShiftStat* stats;            // [batch]
     const double* sigma;         // [batch]
+    const double* alpha;         // [batch] the front assembles alpha A - sigma B (1 except for B-solves)
     double u;                    // threshold pivoting parameter
     // fast path (kernels_front.cu): per-front pivot records and redo flags
     double* aux;                 // [batch][aux_stride]
@@ -115,6 +116,14 @@ void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, i
 void launch_fwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
 void launch_bwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
 int solve_max_front();
+// kth.cu: Lanczos building blocks
+void launch_spmv2(const int64_t* rp, const int32_t* ci, const double* va, const double* vb, const double* x, double* ya,
+                  double* yb, int64_t n, cudaStream_t st);
+void launch_gemv_t(const double* V, int64_t ldv, int j, const double* r, int64_t n, double* out, cudaStream_t st);
+void launch_combine(const double* V, int64_t ldv, int j, const double* c, double cv, double beta_y, double* y,
+                    double a1, const double* x1, double a2, const double* x2, int64_t n, cudaStream_t st);
+void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const double* r, const double* g, int m,
+                 double* X, int64_t ldx, int64_t n, cudaStream_t st);
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 int front_nb_for(int qmax);           // block width for a level (0: too large, use the reference kernel)
@@ -124,4 +133,9 @@ void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, in
 void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st);
 void launch_reset_stats(ShiftStat* st, int batch, cudaStream_t s);
 
+}  // namespace kep
+
+#include <vector>
+namespace kep {
+bool tridiag_eigen(std::vector<double>& d, std::vector<double> e, std::vector<double>& Z);
 }  // namespace kep

@@ -143,13 +143,13 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
     for (int j = warp; j < ld; j += nw)
         for (int i = j + lane; i < ld; i += 32) F[i + (size_t)j * ld] = 0.0;
     __syncthreads();
-    const double sigma = P.sigma[sh];
+    const double sigma = P.sigma[sh], alpha = P.alpha[sh];
     double mx = 0.0;
     for (int64_t k = P.asm_ptr[s] + threadIdx.x; k < P.asm_ptr[s + 1]; k += kAsmThreads) {
         const uint32_t rc = P.asm_rc[k];
         const int lr = (int)(rc >> 16), lc = (int)(rc & 0xffffu);
         const int r = lr < p ? lr : lr + nd;
-        const double v = fma(-sigma, P.b[k], P.a[k]);
+        const double v = fma(-sigma, P.b[k], alpha * P.a[k]);      // alpha A - sigma B (alpha = 1: A - sigma B)
         F[r + (size_t)lc * ld] = v;
         mx = fmax(mx, fabs(v));
     }

@@ -62,6 +62,22 @@ class _FStats(C.Structure):
                 ("nnz_L", C.c_int64), ("store_bytes", C.c_int64)]
 
 
+class _KthOpts(C.Structure):
+    _fields_ = [("m_max", C.c_int32), ("tau_res", C.c_double), ("tau_diff", C.c_double),
+                ("max_lanczos", C.c_int32), ("max_bisect", C.c_int32), ("max_si", C.c_int32),
+                ("shifts_per_round", C.c_int32), ("seed", C.c_uint64),
+                ("v0_stage1", C.POINTER(C.c_double)), ("v0_stage3", C.POINTER(C.c_double))]
+
+
+class _KthReport(C.Structure):
+    _fields_ = [("s1_lower", C.c_double), ("s1_upper", C.c_double), ("s1_nu_lower", C.c_int64),
+                ("s1_nu_upper", C.c_int64), ("sigma_lower", C.c_double), ("sigma_upper", C.c_double),
+                ("nu_lower", C.c_int64), ("nu_upper", C.c_int64), ("sigma_si", C.c_double),
+                ("stage1_iters", C.c_int32), ("stage2_rounds", C.c_int32), ("stage2_shifts", C.c_int32),
+                ("stage3_iters", C.c_int32), ("eta", C.c_double), ("rel_residual", C.c_double),
+                ("rel_diff", C.c_double), ("seconds", C.c_double * 3), ("status", C.c_int)]
+
+
 _lib = None
 
 
@@ -92,6 +108,13 @@ def lib():
         L.kep_last_error.restype = C.c_char_p
         L.kep_version.restype = C.c_char_p
         L.kep_factor.argtypes = [C.c_void_p, C.c_double, P(C.c_void_p)]
+        L.kep_factor_pencil.argtypes = [C.c_void_p, C.c_double, C.c_double, P(C.c_void_p)]
+        L.kep_factor_pencil.restype = C.c_int
+        L.kep_default_kth_opts.argtypes = [P(_KthOpts)]
+        L.kep_default_kth_opts.restype = None
+        L.kep_kth_eigenpair.argtypes = [C.c_void_p, C.c_int64, P(_KthOpts), P(C.c_double), P(C.c_double),
+                                        P(_KthReport)]
+        L.kep_kth_eigenpair.restype = C.c_int
         L.kep_factor_info.argtypes = [C.c_void_p, P(_FStats)]
         L.kep_solve.argtypes = [C.c_void_p, C.c_int32, P(C.c_double), C.c_int64, P(C.c_double), C.c_int64]
         L.kep_solve_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -239,6 +262,39 @@ class Kep:
         h = C.c_void_p()
         self._check(lib().kep_factor(self._h, float(sigma), C.byref(h)))
         return Factor(self, h)
+
+    def factor_pencil(self, alpha: float, sigma: float) -> "Factor":
+        """Retained LDL^T of alpha A - sigma B (alpha = 0, sigma = -1: B)."""
+        h = C.c_void_p()
+        self._check(lib().kep_factor_pencil(self._h, float(alpha), float(sigma), C.byref(h)))
+        return Factor(self, h)
+
+    def kth_eigenpair(self, k: int, m_max=20, tau_res=1e-10, tau_diff=1e-10, max_lanczos=64, max_bisect=128,
+                      max_si=500, shifts_per_round=1, seed=1, v0_stage1=None, v0_stage3=None, want_x=True):
+        """kep_kth_eigenpair: (lambda_k or None, x or None, report dict)."""
+        o = _KthOpts()
+        lib().kep_default_kth_opts(C.byref(o))
+        o.m_max, o.tau_res, o.tau_diff = int(m_max), float(tau_res), float(tau_diff)
+        o.max_lanczos, o.max_bisect, o.max_si = int(max_lanczos), int(max_bisect), int(max_si)
+        o.shifts_per_round, o.seed = int(shifts_per_round), int(seed)
+        keep = []
+        for name, v in (("v0_stage1", v0_stage1), ("v0_stage3", v0_stage3)):
+            if v is not None:
+                arr = np.ascontiguousarray(v, dtype=np.float64)
+                assert arr.shape == (self.n,)
+                keep.append(arr)
+                setattr(o, name, _ptr(arr, C.c_double))
+        lam = C.c_double(np.nan)
+        x = np.empty(self.n) if want_x else None
+        rp = _KthReport()
+        st = lib().kep_kth_eigenpair(self._h, int(k), C.byref(o), C.byref(lam),
+                                     _ptr(x, C.c_double) if want_x else C.cast(None, C.POINTER(C.c_double)),
+                                     C.byref(rp))
+        self._check(st)
+        rep = {f: getattr(rp, f) for f, _ in _KthReport._fields_ if f != "seconds"}
+        rep["seconds"] = list(rp.seconds)
+        ok = rp.status == KEP_OK
+        return (lam.value if ok else None), (x if ok else None), rep
 
     def perm(self) -> np.ndarray:
         p = np.empty(self.n, dtype=np.int64)

@@ -1,0 +1,96 @@
+"""GPU: the three-stage k-th eigenpair driver against
+the oracle (oracle/lanczos.py, LAPACK eigh, closed-form twins).
+
+Bars (BASELINE north_star): lambda_k within 1e-10 relative of the dense result
+(c1) or the closed form (twins), index validated by nu(lambda - d) < k <= nu(lambda + d);
+stage 1 reproduces oracle Alg. 2 from the same start vector (shifts to 1e-9
+relative, counts exact); stage 3 reproduces oracle Alg. 3 on the same interval.
+"""
+import numpy as np
+import pytest
+
+import kepgen
+import oracle
+import oracle.bisection
+from paper_1710_05134_b200 import Kep
+from paper_1710_05134_b200.kep import KEP_OK
+
+pytestmark = pytest.mark.gpu
+
+
+def _start(n, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+def _validate_index(k, p, lam, k_idx):
+    d = 1e-9 * max(1.0, abs(lam))
+    st1, nu1, _ = k.inertia(lam - d)
+    st2, nu2, _ = k.inertia(lam + d)
+    assert st1 == KEP_OK and st2 == KEP_OK
+    assert nu1 < k_idx <= nu2
+
+
+@pytest.mark.parametrize("kk,P", [(300, 1), (300, 4), (37, 1), (812, 2)])
+def test_c1_kth_vs_eigh_and_oracle(kk, P):
+    p = kepgen.config(1)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    v1, v3 = _start(p.n, 11), _start(p.n, 12)
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    lam, x, rep = k.kth_eigenpair(kk, shifts_per_round=P, v0_stage1=v1, v0_stage3=v3)
+    assert rep["status"] == KEP_OK, rep
+    assert abs(lam - w[kk - 1]) <= 1e-10 * abs(w[kk - 1]), (lam, w[kk - 1])
+    _validate_index(k, p, lam, kk)
+    assert np.linalg.norm(A @ x - lam * (B @ x)) / np.linalg.norm(x) < 1e-9
+    assert abs(x @ B @ x - 1.0) < 1e-10
+    # stage 1 == oracle Alg. 2 from the same start vector
+    nu = lambda s: oracle.nu_eig(A, B, s, eigvals=w)
+    lo, hi, nl, nh, j, _ = oracle.initial_interval_alg2(A, B, kk, v1, nu)
+    assert rep["stage1_iters"] == j
+    assert (rep["s1_nu_lower"], rep["s1_nu_upper"]) == (nl, nh)
+    assert np.isclose(rep["s1_lower"], lo, rtol=1e-9) and np.isclose(rep["s1_upper"], hi, rtol=1e-9)
+    assert rep["nu_upper"] - rep["nu_lower"] <= 20 and rep["nu_lower"] < kk <= rep["nu_upper"]
+    if P == 1:     # stage 2 == oracle Alg. 1' and stage 3 == oracle Alg. 3 on the same interval
+        (l2, h2, nl2, nh2), it, _ = oracle.bisection.bisect_alg1p(nu, kk, lo, hi, nl, nh, m_max=20)
+        assert (rep["nu_lower"], rep["nu_upper"]) == (nl2, nh2) and rep["stage2_rounds"] == it
+        res = oracle.si_lanczos_alg3(A, B, kk, l2, h2, nl2, nh2, v3)
+        assert abs(res.lam - lam) <= 1e-11 * abs(lam)
+        assert abs(res.j - rep["stage3_iters"]) <= 2
+
+
+def test_twin_kth_closed_form():
+    q = kepgen.twin_pencil((5, 6, 7), 4, seed=103, uA=0.0, uB=0.01)     # distinct axis lengths: few degeneracies
+    w = oracle.twin_eigenvalues(q.meta["twin"])
+    k = Kep.from_pencil(q)
+    k.set_values(q.a, q.b)
+    for kk in (int(0.25 * q.n), int(0.4 * q.n)):
+        gaps = np.diff(w)
+        if min(gaps[kk - 2], gaps[kk - 1]) < 1e-9 * np.abs(w).max():
+            continue                                    # degenerate lambda_k: not unique
+        lam, x, rep = k.kth_eigenpair(kk)
+        inside = w[rep["nu_lower"]:rep["nu_upper"]]
+        if np.min(np.diff(inside)) < 1e-12 * np.abs(w).max():
+            assert rep["status"] != KEP_OK          # a multiple eigenvalue in the interval: reported, not returned
+            continue
+        assert rep["status"] == KEP_OK, rep
+        assert abs(lam - w[kk - 1]) <= 1e-10 * abs(w[kk - 1])
+        _validate_index(k, q, lam, kk)
+
+
+def test_c2_kth_validated():
+    p = kepgen.config(2)
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    kk = int(0.3 * p.n)
+    lam, x, rep = k.kth_eigenpair(kk, shifts_per_round=8)
+    assert rep["status"] == KEP_OK, rep
+    _validate_index(k, p, lam, kk)
+    import scipy.sparse as sp
+    n = p.n
+    Lo_a = sp.csc_matrix((p.a, p.rowidx, p.colptr), shape=(n, n))
+    Lo_b = sp.csc_matrix((p.b, p.rowidx, p.colptr), shape=(n, n))
+    Af = Lo_a + sp.tril(Lo_a, -1).T
+    Bf = Lo_b + sp.tril(Lo_b, -1).T
+    assert np.linalg.norm(Af @ x - lam * (Bf @ x)) / np.linalg.norm(x) < 1e-9
+    assert rep["eta"] <= 1e-10 * abs(lam) + 1e-14
