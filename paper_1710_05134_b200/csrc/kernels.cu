@@ -16,6 +16,7 @@
 // After a3 the eliminated pivots sit in [0, e), the columns this front delays
 // in [e, p+nd) and the CB rows are untouched in place, so the trailing block
 // F[e:, e:] is exactly what the parent extend-adds.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstdint>
@@ -92,9 +93,30 @@ __device__ __forceinline__ double symget(const double* F, int ld, int i, int j) 
 
 // ---------------------------------------------------------------- a1 + a2
 constexpr int kAsmThreads = 256;
+constexpr int kAsmMapMax = 8192;          // child CB positions staged in shared memory
 
-__global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_begin) {
-    const int s = P.level_fronts[lvl_begin + blockIdx.x];
+// Columns [lo, hi) of a lower triangle of order ld holding the x-th of S equal
+// shares of its entries (column j has ld - j entries).
+__device__ __forceinline__ void tri_split(int ld, int S, int x, int& lo, int& hi) {
+    auto col_at = [&](int y) -> int {
+        if (y <= 0) return 0;
+        if (y >= S) return ld;
+        const double T = 0.5 * (double)ld * (double)(ld + 1), A = T * (double)y / (double)S;
+        const double b = (double)ld + 0.5;
+        int j = (int)ceil(b - sqrt(fmax(b * b - 2.0 * A, 0.0)));
+        return min(max(j, 0), ld);
+    };
+    lo = col_at(x);
+    hi = col_at(x + 1);
+}
+
+// One front of a level, S CTAs per front (blockIdx.x = front * S + x): CTA x
+// owns the parent columns [lo, hi): zero-fill, original entries (alpha a - sigma b),
+// then the children's CB entries landing in those columns, children in order.
+// Each parent entry belongs to one CTA, so the sum order is fixed (deterministic).
+__global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_begin, int S) {
+    const int s = P.level_fronts[lvl_begin + blockIdx.x / S];
+    const int xs = blockIdx.x % S;
     const int sh = blockIdx.y;
     ShiftStat* st = P.stats + sh;
     double* arena = P.arena + (size_t)sh * P.arena_stride;
@@ -103,6 +125,7 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
     int32_t* doff = P.doff + (size_t)sh * P.nf;
     __shared__ int s_nd, s_skip;
     __shared__ double s_red[32];
+    __shared__ int s_pos[kAsmMapMax];
     const int c0 = P.child_ptr[s], c1 = P.child_ptr[s + 1];
     if (threadIdx.x == 0) {
         int off = 0, bad = 0;
@@ -110,37 +133,41 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
             const int c = P.child_list[q];
             const int no = nd_out[c];
             if (no < 0) bad = 1;
-            doff[c] = off;
+            if (xs == 0) doff[c] = off;
             off += no > 0 ? no : 0;
         }
         const int need = P.forder[s] + off;
         if (need > P.cap[s]) {
             bad = 1;
-            atomicMax(&st->need_slack, off);
+            if (xs == 0) atomicMax(&st->need_slack, off);
         }
-        if (bad) atomicOr(&st->flags, FLAG_OVERFLOW);
+        if (bad && xs == 0) atomicOr(&st->flags, FLAG_OVERFLOW);
         s_skip = bad;
         s_nd = off;
-        nd_in[s] = bad ? -1 : off;
+        if (xs == 0) nd_in[s] = bad ? -1 : off;
     }
     __syncthreads();
     if (s_skip) return;
     const int nd = s_nd, p = P.npiv[s], ld = P.forder[s] + nd;
     double* F = arena + P.arena_off[s];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAsmThreads / 32;
-    {   // labels of the FS positions: own pivots, then each child's delayed variables
+    int clo, chi;
+    tri_split(ld, S, xs, clo, chi);
+    if (xs == 0) {   // labels of the FS positions: own pivots, then each child's delayed variables
         const AuxRec A = aux_rec(P, sh, s, P.cap[s] - P.ncb[s]);
         for (int i = threadIdx.x; i < p; i += kAsmThreads) A.label[i] = P.piv_first[s] + i;
+        int off = 0;
         for (int q = c0; q < c1; ++q) {
             const int c = P.child_list[q];
             const int ndo = nd_out[c];
             if (ndo <= 0) continue;
             const AuxRec C = aux_rec(P, sh, c, P.cap[c] - P.ncb[c]);
             const int ec = P.npiv[c] + nd_in[c] - ndo;
-            for (int j = threadIdx.x; j < ndo; j += kAsmThreads) A.label[p + doff[c] + j] = C.label[C.perm[ec + j]];
+            for (int j = threadIdx.x; j < ndo; j += kAsmThreads) A.label[p + off + j] = C.label[C.perm[ec + j]];
+            off += ndo;
         }
     }
-    for (int j = warp; j < ld; j += nw)
+    for (int j = clo + warp; j < chi; j += nw)
         for (int i = j + lane; i < ld; i += 32) F[i + (size_t)j * ld] = 0.0;
     __syncthreads();
     const double sigma = P.sigma[sh], alpha = P.alpha[sh];
@@ -148,14 +175,16 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
     for (int64_t k = P.asm_ptr[s] + threadIdx.x; k < P.asm_ptr[s + 1]; k += kAsmThreads) {
         const uint32_t rc = P.asm_rc[k];
         const int lr = (int)(rc >> 16), lc = (int)(rc & 0xffffu);
+        if (lc < clo || lc >= chi) continue;
         const int r = lr < p ? lr : lr + nd;
         const double v = fma(-sigma, P.b[k], alpha * P.a[k]);      // alpha A - sigma B (alpha = 1: A - sigma B)
         F[r + (size_t)lc * ld] = v;
         mx = fmax(mx, fabs(v));
     }
     mx = block_max<kAsmThreads>(mx, s_red);
-    if (threadIdx.x == 0) atomic_max_pos_double(&st->smax_bits, mx);
-    // a2: extend-add, children in a fixed order (deterministic, no float atomics)
+    if (threadIdx.x == 0 && mx > 0.0) atomic_max_pos_double(&st->smax_bits, mx);
+    // a2: extend-add, children in a fixed order
+    int off = 0;
     for (int q = c0; q < c1; ++q) {
         const int c = P.child_list[q];
         const int ndo = nd_out[c];
@@ -165,15 +194,30 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
         const double* __restrict__ Fc = arena + P.arena_off[c];
         double* __restrict__ Fp = F;
         const int32_t* __restrict__ rm = P.rmap + P.rmap_ptr[c];
-        const int dof = p + doff[c];
-        auto pos = [&](int x) -> int {                 // child CB index -> parent position
+        const int dof = p + off;
+        off += ndo > 0 ? ndo : 0;
+        const bool staged = mc <= kAsmMapMax;
+        __syncthreads();                                         // s_pos reuse
+        if (staged)
+            for (int x = threadIdx.x; x < mc; x += kAsmThreads) {
+                int v;
+                if (x < ndo) v = dof + x;
+                else { const int r = rm[x - ndo]; v = r < p ? r : r + nd; }
+                s_pos[x] = v;
+            }
+        __syncthreads();
+        auto pos = [&](int x) -> int {
+            if (staged) return s_pos[x];
             if (x < ndo) return dof + x;
             const int r = rm[x - ndo];
             return r < p ? r : r + nd;
         };
-        constexpr int U = 4;                           // rows in flight per lane
+        constexpr int U = 4;                                     // rows in flight per lane
         for (int j = warp; j < mc; j += nw) {
             const int pj = pos(j);
+            // non-delayed child columns land in parent column pj (positions increase with the
+            // child index there); delayed columns are filtered entry by entry
+            if (j >= ndo && (pj < clo || pj >= chi)) continue;
             const double* __restrict__ colc = Fc + (size_t)(ec + j) * fc + ec;
             for (int i0 = j; i0 < mc; i0 += 32 * U) {
                 double v[U];
@@ -186,8 +230,10 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
                     if (i < mc) {
                         const int pi = pos(i);
                         const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
-                        dst[u] = hi + (size_t)lo * ld;
-                        v[u] = colc[i];
+                        if (lo >= clo && lo < chi) {
+                            dst[u] = hi + (size_t)lo * ld;
+                            v[u] = colc[i];
+                        }
                     }
                 }
                 double old[U];
@@ -198,7 +244,6 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
                     if (dst[u] != SIZE_MAX) Fp[dst[u]] = old[u] + v[u];
             }
         }
-        __syncthreads();
     }
 }
 
@@ -413,7 +458,10 @@ __global__ void k_reset_stats(ShiftStat* st, int batch) {
 }  // namespace
 
 void launch_assemble(const DevPlan& P, int lvl_begin, int nfronts, int batch, cudaStream_t st) {
-    k_assemble<<<dim3(nfronts, batch), kAsmThreads, 0, st>>>(P, lvl_begin);
+    // CTAs per front: enough to give ~4 resident CTAs per SM on the whole level
+    int S = (int)((4 * 148 + (int64_t)nfronts * batch - 1) / ((int64_t)nfronts * batch));
+    S = std::max(1, std::min(S, 16));
+    k_assemble<<<dim3(nfronts * S, batch), kAsmThreads, 0, st>>>(P, lvl_begin, S);
 }
 
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,

@@ -49,8 +49,8 @@ namespace {
 
 constexpr double kAlpha = 0.6403882032022076;   // (1 + sqrt(17)) / 8
 constexpr int FT = 256;                         // k_fs / k_check threads
-constexpr int LT = 128;                         // k_l21 threads (4 warps x 16 rows)
-constexpr int LR = 64;                          // k_l21 CB rows per CTA
+constexpr int LT = 256;                         // k_l21 threads (8 warps x 16 rows)
+constexpr int LR = 128;                         // k_l21 CB rows per CTA
 constexpr int LB = 32;                          // k_l21 column block
 constexpr int KC = 16;                          // K chunk of the k_l21 GEMM
 constexpr int APAD = LR + 4;                    // = 4 (mod 16): conflict-free f64 fragments
@@ -67,11 +67,12 @@ __device__ __forceinline__ MaxIdx better(MaxIdx a, MaxIdx b) {
 }
 
 struct Red {
-    MaxIdx mi[FT / 32];
-    double x[3][FT / 32];
+    MaxIdx mi[8];
+    double x[3][8];
 };
 
 // block-wide (max, argmax) of a and max of b, c, d
+template <int TH>
 __device__ void block_reduce(MaxIdx& a, double& b, double& c, double& d, Red* R) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -89,7 +90,7 @@ __device__ void block_reduce(MaxIdx& a, double& b, double& c, double& d, Red* R)
     __syncthreads();
     a = R->mi[0]; b = R->x[0][0]; c = R->x[1][0]; d = R->x[2][0];
 #pragma unroll
-    for (int q = 1; q < FT / 32; ++q) {
+    for (int q = 1; q < TH / 32; ++q) {
         a = better(a, R->mi[q]);
         b = fmax(b, R->x[0][q]);
         c = fmax(c, R->x[1][q]);
@@ -114,9 +115,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // Symmetric interchange of FS positions a < b in the lower FS x FS block
 // (rows/columns of the active part and L rows of the columns t < a).
+template <int TH>
 __device__ void sym_swap_fs(double* F, int ld, int q, int a, int b) {
     if (a == b) return;
-    for (int t = threadIdx.x; t < q; t += FT) {
+    for (int t = threadIdx.x; t < q; t += TH) {
         if (t < a) {
             double* x = F + a + (size_t)t * ld;
             double* y = F + b + (size_t)t * ld;
@@ -200,12 +202,12 @@ __device__ __forceinline__ double wform(const Smem<NB>& S, int RS, int t, int ii
 // After the global interchange of positions a < b: L rows a, b of all block
 // columns (raw ones included), whole raw columns a, b reloaded, rows a, b of
 // the other raw columns reloaded.  kfirst = first raw (not yet pivoted) column.
-template <int NB>
+template <int NB, int TH>
 __device__ void swap_block(const Smem<NB>& S, int RS, const double* F, int ld, int q, int kp, int kfirst, int a, int b,
                            int* perm) {
     const int tid = threadIdx.x;
     __syncthreads();                                   // global interchange complete
-    for (int t = tid; t < NB; t += FT) {
+    for (int t = tid; t < NB; t += TH) {
         double* col = S.Ls + (size_t)t * RS;
         const double x = col[a - kp];
         col[a - kp] = col[b - kp];
@@ -214,7 +216,7 @@ __device__ void swap_block(const Smem<NB>& S, int RS, const double* F, int ld, i
     if (tid == 0) { const int x = perm[a]; perm[a] = perm[b]; perm[b] = x; }
     __syncthreads();
     const int hi = min(kp + NB, q);
-    for (int j = kfirst + tid; j < hi; j += FT) {
+    for (int j = kfirst + tid; j < hi; j += TH) {
         if (j == a || j == b) continue;
         double* col = S.Ls + (size_t)(j - kp) * RS;
         if (a >= j) col[a - kp] = F[a + (size_t)j * ld];
@@ -225,23 +227,24 @@ __device__ void swap_block(const Smem<NB>& S, int RS, const double* F, int ld, i
         const int j = cols[x];
         if (j < kfirst || j >= hi) continue;
         double* col = S.Ls + (size_t)(j - kp) * RS;
-        for (int i = j + tid; i < q; i += FT) col[i - kp] = F[i + (size_t)j * ld];
+        for (int i = j + tid; i < q; i += TH) col[i - kp] = F[i + (size_t)j * ld];
     }
     __syncthreads();
 }
 
-template <int NB>
+template <int NB, int TH>
 __device__ void do_swap(const Smem<NB>& S, int RS, double* F, int ld, int q, int kp, int kfirst, int a, int b, int* perm) {
     if (a == b) return;
-    sym_swap_fs(F, ld, q, a, b);
-    swap_block<NB>(S, RS, F, ld, q, kp, kfirst, a, b, perm);
+    sym_swap_fs<TH>(F, ld, q, a, b);
+    swap_block<NB, TH>(S, RS, F, ld, q, kp, kfirst, a, b, perm);
 }
 
-template <int NB>
 // One block of at most NB pivots per launch (mode 0: first block of pass 0;
 // mode 1: first block of a rerun pass; mode 2: next block).  The state between
 // launches (e, qe, S1 step, forced-delay cursor, block start) lives in fstate.
-__global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restrict__ fronts, int RS, int mode) {
+// TH threads per front (one warp for tiny FS blocks).
+template <int NB, int TH>
+__global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict__ fronts, int RS, int mode) {
     extern __shared__ __align__(16) double dyn[];
     const Smem<NB> S = carve<NB>(dyn, RS);
     const int s = fronts[blockIdx.x];
@@ -287,12 +290,12 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
     if (mode < 2) {
         // keep the assembled A11 (strict lower -> upper, diagonal -> aux) for a restore
         if (!root) {
-            for (int j = warp; j < q; j += FT / 32) {
+            for (int j = warp; j < q; j += TH / 32) {
                 for (int i = j + 1 + lane; i < q; i += 32) F[j + (size_t)i * ld] = F[i + (size_t)j * ld];
                 if (lane == 0) A.diag[j] = F[j + (size_t)j * ld];
             }
         }
-        for (int i = tid; i < q; i += FT) { A.perm[i] = i; A.cm[i] = 0ull; }
+        for (int i = tid; i < q; i += TH) { A.perm[i] = i; A.cm[i] = 0ull; }
     } else {
         e = fst[0]; qe = fst[1]; step = fst[2]; fnext = fst[3];
     }
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
     {
         {   // raw block columns [kp, kp+NB), rows [j, q)
             const int npre = min(NB, q - kp), R = q - kp;
-            for (int idx = tid; idx < npre * R; idx += FT) {
+            for (int idx = tid; idx < npre * R; idx += TH) {
                 const int x = idx / R, ii = idx - x * R;
                 if (ii >= x) S.Ls[(size_t)x * RS + ii] = F[(kp + ii) + (size_t)(kp + x) * ld];
             }
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
             const int k = e, t = k - kp;
             if (fnext < s_forced[0] && step == s_forced[1 + fnext]) {
                 // the full-column test failed here in an earlier pass: delay (R1)
-                do_swap<NB>(S, RS, F, ld, q, kp, k, k, qe - 1, A.perm);
+                do_swap<NB, TH>(S, RS, F, ld, q, kp, k, k, qe - 1, A.perm);
                 qe--;
                 fnext++;
                 step++;
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
             double mR = 0.0, z1 = 0.0, z2 = 0.0;
             {
                 const double* raw = S.Ls + (size_t)t * RS;
-                for (int i = k + tid; i < q; i += FT) {
+                for (int i = k + tid; i < q; i += TH) {
                     const int ii = i - kp;
                     double v = raw[ii];
                     for (int x = 0; x < t; ++x) v = fma(-S.Ls[(size_t)x * RS + ii], S.wrow[x], v);
@@ -335,14 +338,14 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
                     }
                 }
             }
-            block_reduce(mC, mR, z1, z2, S.red);
+            block_reduce<TH>(mC, mR, z1, z2, S.red);
             const double gC = mC.v > 0.0 ? mC.v : 0.0;
             const int r = mC.v >= 0.0 ? mC.i : k;
             const double akk = fabs(S.wk[k - kp]);
             if (akk == 0.0 && mR == 0.0) {
                 // FS part of column k is zero: a zero pivot if its CB part is
                 // zero too (k_check), else the unblocked rule delays it there
-                for (int i = k + tid; i < q; i += FT) S.Ls[(size_t)t * RS + (i - kp)] = 0.0;
+                for (int i = k + tid; i < q; i += TH) S.Ls[(size_t)t * RS + (i - kp)] = 0.0;
                 if (tid == 0) {
                     S.cs[t] = 0.0; S.co[t] = 0.0; S.oo[t] = 0; S.tp[t] = PK_ZERO;
                     S.d1[t] = 0.0; S.d2[t] = 0.0; S.fa[t] = 0.0; S.fb[t] = 0.0; S.st[t] = step;
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
                 __syncthreads();
                 double mc = 0.0, ma = 0.0, m3 = 0.0;
                 MaxIdx dm{-1.0, INT_MAX};
-                for (int i = k + tid; i < q; i += FT) {
+                for (int i = k + tid; i < q; i += TH) {
                     const int ii = i - kp;
                     double v = i >= r ? F[i + (size_t)r * ld] : F[r + (size_t)i * ld];
                     for (int x = 0; x < t; ++x) v = fma(-S.Ls[(size_t)x * RS + ii], S.wrowr[x], v);
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
                         if (i != k) { ma = fmax(ma, a); m3 = fmax(m3, fabs(S.wk[ii])); }
                     }
                 }
-                block_reduce(dm, mc, ma, m3, S.red);
+                block_reduce<TH>(dm, mc, ma, m3, S.red);
                 const double rho = mc;                       // includes |a_kr| = gC
                 rall = ma;                                   // column r, rows not in {k, r}
                 gk = m3;                                     // column k, rows not in {k, r}
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
                 }
             }
             if (!ok) {                                      // fails on the FS rows already: delay
-                do_swap<NB>(S, RS, F, ld, q, kp, k, k, qe - 1, A.perm);
+                do_swap<NB, TH>(S, RS, F, ld, q, kp, k, k, qe - 1, A.perm);
                 qe--;
                 step++;
                 continue;
@@ -407,14 +410,14 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
             if (kind == 1) {
                 double* w = S.wk;
                 if (j != k) {
-                    do_swap<NB>(S, RS, F, ld, q, kp, k + 1, k, j, A.perm);
+                    do_swap<NB, TH>(S, RS, F, ld, q, kp, k + 1, k, j, A.perm);
                     if (tid == 0) { const double x = S.wr[k - kp]; S.wr[k - kp] = S.wr[j - kp]; S.wr[j - kp] = x; }
                     __syncthreads();
                     w = S.wr;
                 }
                 const double d = w[k - kp];
                 const double dinv = 1.0 / d;
-                for (int i = k + 1 + tid; i < q; i += FT) S.Ls[(size_t)t * RS + (i - kp)] = w[i - kp] * dinv;
+                for (int i = k + 1 + tid; i < q; i += TH) S.Ls[(size_t)t * RS + (i - kp)] = w[i - kp] * dinv;
                 if (tid == 0) {
                     S.cs[t] = d; S.co[t] = 0.0; S.oo[t] = 0; S.tp[t] = PK_1X1;
                     S.d1[t] = d; S.d2[t] = 0.0; S.fa[t] = fa; S.fb[t] = 0.0; S.st[t] = step;
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
                 e += 1;
                 step++;
             } else {
-                do_swap<NB>(S, RS, F, ld, q, kp, k + 2, k + 1, r, A.perm);
+                do_swap<NB, TH>(S, RS, F, ld, q, kp, k + 2, k + 1, r, A.perm);
                 if (tid == 0) {
                     double x = S.wk[k + 1 - kp]; S.wk[k + 1 - kp] = S.wk[r - kp]; S.wk[r - kp] = x;
                     x = S.wr[k + 1 - kp]; S.wr[k + 1 - kp] = S.wr[r - kp]; S.wr[r - kp] = x;
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
                 const double d11 = S.wk[k - kp], d21 = S.wk[k + 1 - kp], d22 = S.wr[k + 1 - kp];
                 const double det = d11 * d22 - d21 * d21;
                 const double i11 = d22 / det, i21 = -d21 / det, i22 = d11 / det;
-                for (int i = k + 2 + tid; i < q; i += FT) {
+                for (int i = k + 2 + tid; i < q; i += TH) {
                     const double w1 = S.wk[i - kp], w2 = S.wr[i - kp];
                     S.Ls[(size_t)t * RS + (i - kp)] = w1 * i11 + w2 * i21;
                     S.Ls[(size_t)(t + 1) * RS + (i - kp)] = w1 * i21 + w2 * i22;
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(FT, 1) k_fsp(DevPlan P, const int32_t* __restr
         }
         // ---- commit the block: L (FS rows), D and the test record; FS trailing update
         const int nbn = e - kp;
-        for (int t = warp; t < nbn; t += FT / 32) {
+        for (int t = warp; t < nbn; t += TH / 32) {
             const int cpos = kp + t;
             const int o = S.oo[t];
             const int i1 = cpos + 1 + (o == 1 ? 1 : 0);
@@ -554,12 +557,15 @@ __global__ void __launch_bounds__(UT) k_fsu(DevPlan P, const int4* __restrict__ 
 // W21 = A21 P^T L11^-T for 64 CB rows of one front; column maxima of W21.
 // L11[i,t] = 0 for t >= e (delayed columns have no pivot: their W21 column
 // is the fully updated CB part of the delayed column).
-__global__ void __launch_bounds__(LT) k_l21(DevPlan P, const int4* __restrict__ items) {
-    __shared__ __align__(16) double As[2][KC][APAD];
-    __shared__ __align__(16) double Bs[2][LB][BP];
-    static_assert(sizeof(double) * LR * (LB + 1) <= sizeof(double) * 2 * KC * APAD, "Sacc aliases As");
-    double (*Sacc)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(&As[0][0][0]);
-    __shared__ double Lbb[LB][LB + 1];
+__global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict__ items) {
+    extern __shared__ __align__(16) double l21_smem[];
+    double (*As)[KC][APAD] = reinterpret_cast<double (*)[KC][APAD]>(l21_smem);                  // [2][KC][APAD]
+    double (*Bs)[LB][BP] = reinterpret_cast<double (*)[LB][BP]>(l21_smem + 2 * KC * APAD);      // [2][LB][BP]
+    double (*Sbase)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + 2 * KC * APAD + 2 * LB * BP);
+    static_assert(LR * (LB + 1) <= 2 * KC * APAD, "Sacc aliases As");
+    static_assert(LB * (LB + 1) <= 2 * LB * BP, "Lbb aliases Bs");
+    double (*Sacc)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem);
+    double (*Lbb)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + 2 * KC * APAD);
     __shared__ int sperm[LB];
     const int4 it = items[blockIdx.x];
     const int s = it.x, I = it.y;
@@ -580,9 +586,20 @@ __global__ void __launch_bounds__(LT) k_l21(DevPlan P, const int4* __restrict__ 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, tg = lane & 3;
     const int wm = warp * 16;
+    const int row = tid >> 1, half = tid & 1;               // triangle: two threads per CB row
     for (int b0 = 0; b0 < q; b0 += LB) {
         const int nbc = min(LB, q - b0);
         const int K = min(b0, e);
+        if (tid < LB) sperm[tid] = tid < nbc ? A.perm[b0 + tid] : 0;
+        __syncthreads();
+        // gathered A21 columns of the block (A21 P^T), fetched while the GEMM runs
+        for (int x = tid; x < LB * LR; x += LT) {
+            const int t = x / LR, ii = x - t * LR;
+            const int gi = r0 + ii;
+            const bool v = gi < f && t < nbc;
+            cp_async8(&Sbase[ii][t], F + (v ? (gi + (size_t)sperm[t] * ld) : 0), v);
+        }
+        cp_async_commit();
         double acc[2][4][2];
 #pragma unroll
         for (int mb = 0; mb < 2; ++mb)
@@ -629,6 +646,9 @@ __global__ void __launch_bounds__(LT) k_l21(DevPlan P, const int4* __restrict__ 
                 }
                 __syncthreads();
             }
+        } else {
+            cp_async_wait<0>();
+            __syncthreads();
         }
 #pragma unroll
         for (int mb = 0; mb < 2; ++mb)
@@ -636,40 +656,42 @@ __global__ void __launch_bounds__(LT) k_l21(DevPlan P, const int4* __restrict__ 
             for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) Sacc[wm + 8 * mb + g][8 * nb + 2 * tg + h] = acc[mb][nb][h];
-        // diagonal block of L11 (strict lower, columns < e only) and the permutation
+        // diagonal block of L11 (strict lower, columns < e only)
         for (int x = tid; x < LB * LB; x += LT) {
             const int a = x / LB, b = x - a * LB;
             double v = 0.0;
             if (a < nbc && b < a && b0 + b < e) v = F[(b0 + a) + (size_t)(b0 + b) * ld];
             Lbb[a][b] = v;
         }
-        if (tid < LB) sperm[tid] = tid < nbc ? A.perm[b0 + tid] : 0;
         __syncthreads();
-        if (tid < LR) {
-            const int i = r0 + tid;
+        {   // in-block unit-lower solve: thread pair (row, parity) splits each dot product
+            const int i = r0 + row;
             const bool valid = i < f;
-            const double* __restrict__ Fi = F + i;
-            double xr[LB];
-#pragma unroll
-            for (int t = 0; t < LB; ++t)                    // all loads first (no store can alias them)
-                xr[t] = (valid && t < nbc) ? Fi[(size_t)sperm[t] * ld] : 0.0;
+            double xh[LB / 2];
 #pragma unroll
             for (int t = 0; t < LB; ++t) {
-                double v = xr[t] - Sacc[tid][t];
+                double p0 = 0.0, p1 = 0.0;
 #pragma unroll
-                for (int x = 0; x < t; ++x) v = fma(-xr[x], Lbb[t][x], v);
-                xr[t] = t < nbc ? v : 0.0;
+                for (int u = 0; 2 * u + half < t && u < LB / 2; u += 2) {
+                    p0 = fma(xh[u], Lbb[t][2 * u + half], p0);
+                    if (2 * (u + 1) + half < t) p1 = fma(xh[u + 1], Lbb[t][2 * (u + 1) + half], p1);
+                }
+                const double part = p0 + p1;
+                const double tot = part + __shfl_xor_sync(0xffffffffu, part, 1);
+                double v = Sbase[row][t] - Sacc[row][t] - tot;
+                v = (t < nbc && valid) ? v : 0.0;
+                if ((t & 1) == half) xh[t >> 1] = v;
             }
             if (valid) {
                 double* __restrict__ Wi = F + (size_t)i * ld + b0;
 #pragma unroll
-                for (int t = 0; t < LB; ++t)
-                    if (t < nbc) Wi[t] = xr[t];
+                for (int u = 0; u < LB / 2; ++u)
+                    if (2 * u + half < nbc) Wi[2 * u + half] = xh[u];
             }
 #pragma unroll
             for (int t = 0; t < LB; ++t) {
                 if (t < nbc && b0 + t < e) {
-                    double m = valid ? fabs(xr[t]) : 0.0;
+                    double m = ((t & 1) == half) ? fabs(xh[t >> 1]) : 0.0;
 #pragma unroll
                     for (int o2 = 16; o2 > 0; o2 >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o2));
                     if (lane == 0 && m > 0.0) atomicMax(&A.cm[b0 + t], (unsigned long long)__double_as_longlong(m));
@@ -824,7 +846,7 @@ int fs_rows_pad(int qmax) { return ((qmax + 15) / 16) * 16 + 4; }
 int front_nb_for(int qmax) {
     const int RS = fs_rows_pad(qmax);
     const size_t lim = kFsSmemLimit;
-    if (fs_smem_bytes(32, RS) <= lim && qmax <= 384) return 32;
+    if (fs_smem_bytes(32, RS) <= lim && qmax <= 640) return 32;
     if (fs_smem_bytes(16, RS) <= lim) return 16;
     if (fs_smem_bytes(8, RS) <= lim) return 8;
     return 0;
@@ -835,22 +857,29 @@ int fs_iters(int qmax) {
     return nb > 1 ? (qmax + nb - 2) / (nb - 1) + 1 : 0;
 }
 
+template <int NB, int TH>
+void launch_fsp_t(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int RS, size_t smem, int mode,
+                  cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_fsp<NB, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
+        attr = true;
+    }
+    k_fsp<NB, TH><<<dim3(nfronts, batch), TH, smem, st>>>(P, fronts, RS, mode);
+}
+
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st) {
     if (nfronts <= 0) return;
     const int nb = front_nb_for(qmax);
     const int RS = fs_rows_pad(qmax);
     const size_t smem = fs_smem_bytes(nb, RS);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_fsp<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
-        cudaFuncSetAttribute(k_fsp<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
-        cudaFuncSetAttribute(k_fsp<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
-        attr = true;
-    }
-    const dim3 grid(nfronts, batch);
-    if (nb == 32) k_fsp<32><<<grid, FT, smem, st>>>(P, fronts, RS, mode);
-    else if (nb == 16) k_fsp<16><<<grid, FT, smem, st>>>(P, fronts, RS, mode);
-    else k_fsp<8><<<grid, FT, smem, st>>>(P, fronts, RS, mode);
+    // threads per front: one warp for tiny FS blocks (no CTA-wide barriers), 4 or 8 warps above
+    const int th = qmax <= 40 ? 32 : (qmax <= 192 ? 128 : 256);
+#define KEP_FSP(NBV, THV) if (nb == NBV && th == THV) return launch_fsp_t<NBV, THV>(P, fronts, nfronts, batch, RS, smem, mode, st)
+    KEP_FSP(32, 32); KEP_FSP(32, 128); KEP_FSP(32, 256);
+    KEP_FSP(16, 32); KEP_FSP(16, 128); KEP_FSP(16, 256);
+    KEP_FSP(8, 32); KEP_FSP(8, 128); KEP_FSP(8, 256);
+#undef KEP_FSP
 }
 
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
@@ -860,7 +889,10 @@ void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cuda
 
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
     if (nitems <= 0) return;
-    k_l21<<<dim3(nitems, batch), LT, 0, st>>>(P, items);
+    const size_t smem = sizeof(double) * (2 * KC * APAD + 2 * LB * BP + LR * (LB + 1));
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(k_l21, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+    k_l21<<<dim3(nitems, batch), LT, smem, st>>>(P, items);
 }
 
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
