@@ -249,7 +249,7 @@ def main():
     P = world * S
     kk = meta["k"]
     lo0, hi0 = meta["lo"], meta["hi"]
-    state = dict(lo=lo0, hi=hi0, nlo=0, nhi=n, rounds=0, restarts=0)
+    state = dict(lo=lo0, hi=hi0, nlo=0, nhi=n, rounds=0, restarts=0, redo=0, delayed=0, evals=0)
 
     def one_round(set_vals=None):
         """One multisection round: P interior shifts of [lo, hi), this rank takes i = rank mod world."""
@@ -258,7 +258,10 @@ def main():
         lo, hi = state["lo"], state["hi"]
         sig_all = lo + (np.arange(P) + 1.0) * (hi - lo) / (P + 1)
         mine = sig_all[rank::world]
-        nus, st = k.inertia_many(mine)
+        nus, st, infos = k.inertia_many(mine, with_info=True)
+        state["redo"] += sum(i.n_redo for i in infos)
+        state["delayed"] += sum(i.n_delayed for i in infos)
+        state["evals"] += len(infos)
         nus = np.where(st == 0, nus, -1).astype(np.int64)
         if world > 1:
             t = torch.from_numpy(nus).cuda()
@@ -363,7 +366,9 @@ def main():
                            "flops_per_shift_alg": ana["flops"], "factor_tflops_per_gpu": fac_tflops,
                            "factor_tflops_frac_of_fp64_peak": fac_tflops / peak if peak else None,
                            "fronts": ana["n_fronts"], "levels": ana["n_levels"], "max_front": ana["max_front"],
-                           "multisection_rounds": state["rounds"], "restarts": state["restarts"]},
+                           "multisection_rounds": state["rounds"], "restarts": state["restarts"],
+                           "delayed_pivots_per_shift": state["delayed"] / max(state["evals"], 1),
+                           "fast_path_reruns_per_shift": state["redo"] / max(state["evals"], 1)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": _clock_summary(clocks), "wall_s": wall,
                 "setup_s": {"generate": t_gen, "analyze": t_an}}

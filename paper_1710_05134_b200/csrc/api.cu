@@ -205,7 +205,7 @@ kep_status build_lists(kep_ctx* c) {
             if (use_fast && kep::front_nb_for(qcap) > 0) {
                 fast.push_back(s);
                 c->level_qmax[L] = std::max(c->level_qmax[L], qcap);
-                for (int I = 0; I < (S.ncb[s] + 63) / 64; ++I) litems.push_back(make_int4(s, I, 0, 0));
+                for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) litems.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
                 for (int I = 0; I < (qcap + 63) / 64; ++I)
                     for (int J = 0; J <= I; ++J) uitems.push_back(make_int4(s, I, J, 0));
                 const int nt = (S.ncb[s] + 63) / 64;
@@ -476,16 +476,21 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                             c->prof.launches[KEP_K_FSU]++;
                         }
                     }
+                    mark(KEP_K_L21, true);
+                    kep::launch_prep(P, fl, nfl2, m, c->stream);            // L11 -> B' = L11 D M^-T (every fast front)
+                    mark(KEP_K_L21, false);
+                    c->prof.launches[KEP_K_L21]++;
                     if (c->litem_cnt[L]) {
                         mark(KEP_K_L21, true);
                         kep::launch_l21(P, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, c->stream);
                         mark(KEP_K_L21, false);
-                        c->prof.launches[KEP_K_L21]++;
+                        c->prof.launches[KEP_K_L21] += 1;
                     }
                     mark(KEP_K_CHECK, true);
                     kep::launch_check(P, fl, nfl2, m, c->stream);
+                    kep::launch_restore(P, fl, nfl2, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, c->stream);
                     mark(KEP_K_CHECK, false);
-                    c->prof.launches[KEP_K_CHECK]++;
+                    c->prof.launches[KEP_K_CHECK] += 3;
                 }
                 mark(KEP_K_REF, true);
                 kep::launch_factor_list(P, fl, nfl2, m, c->stream, true);

@@ -59,7 +59,8 @@ struct DevPlan {
 
 // pivot kinds recorded per eliminated position
 constexpr int PK_1X1 = 0, PK_2X2A = 1, PK_2X2B = 2, PK_ZERO = 3;
-constexpr int AUX_W = 8;         // doubles per position: diag backup, d, ds, fa, fb, cm, (kind, perm), (step, -)
+constexpr int AUX_W = 13;        // doubles per position: diag backup, d, ds, fa, fb, cm, (kind, perm), (step, label),
+                                 // sgn, gca, gcb, hca, hcb
 // front states: FL_OK = factorised, FL_REF = hand to the unblocked kernel,
 // FL_RERUN = rerun the fast path with one more forced delay, FL_ACTIVE = in the current fast pass
 constexpr int FL_OK = 0, FL_REF = 1, FL_RERUN = 2, FL_ACTIVE = 3;
@@ -71,6 +72,9 @@ struct AuxRec {
     unsigned long long* cm;      // CB column maxima of W21 (positive-double bits)
     int *kind, *perm, *step;
     int* label;                  // assembly-order variable (elimination position) of each FS position
+    double* sgn;                 // +-1: sign of the eigenvalue of D carried by the G column (k_schur)
+    double *gca, *gcb;           // G[:, t] = W21[:, t] gca[t] + W21[:, t +- 1] gcb[t] (2x2 partner)
+    double *hca, *hcb;           // (L11 D M^-T)[:, t] = L11[:, t] hca[t] + L11[:, t +- 1] hcb[t], so G B'^T = W21 L11^T
 };
 
 __device__ __forceinline__ AuxRec aux_rec(const DevPlan& P, int sh, int s, int Q) {
@@ -82,7 +86,26 @@ __device__ __forceinline__ AuxRec aux_rec(const DevPlan& P, int sh, int s, int Q
     A.perm = A.kind + Q;
     A.step = (int*)(b + 7 * Q);
     A.label = A.step + Q;
+    A.sgn = b + 8 * Q;
+    A.gca = b + 9 * Q;
+    A.gcb = b + 10 * Q;
+    A.hca = b + 11 * Q;
+    A.hcb = b + 12 * Q;
     return A;
+}
+
+// Eigen-decomposition of a 2x2 pivot block D = [d11 d21; d21 d22] = Q diag(l1, l2) Q^T,
+// Q = [cs -sn; sn cs] (Jacobi rotation).  With it the Schur update of a front is
+// W21 D^-1 W21^T = G S G^T,  G = W21 Q |Lambda|^-1/2 S,  S = sign(Lambda)
+// (1x1 pivots: G = W21 sign(d) / sqrt|d|), so k_schur multiplies G by G with sign
+// flips only.
+__device__ __forceinline__ void pair_eig(double d11, double d21, double d22, double& cs, double& sn, double& l1,
+                                         double& l2) {
+    const double th = 0.5 * atan2(2.0 * d21, d11 - d22);
+    cs = cos(th);
+    sn = sin(th);
+    l1 = d11 * cs * cs + 2.0 * d21 * cs * sn + d22 * sn * sn;
+    l2 = d11 * sn * sn - 2.0 * d21 * cs * sn + d22 * cs * cs;
 }
 
 __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
@@ -125,7 +148,10 @@ void launch_combine(const double* V, int64_t ldv, int j, const double* c, double
 void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const double* r, const double* g, int m,
                  double* X, int64_t ldx, int64_t n, cudaStream_t st);
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
+void launch_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
+void launch_restore(const DevPlan& P, const int32_t* fronts, int nfronts, const int4* litems, int nlitems, int batch,
+                    cudaStream_t st);
 int front_nb_for(int qmax);           // block width for a level (0: too large, use the reference kernel)
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,

@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
         const int ec = fc - mc;
         const double* __restrict__ Fc = arena + P.arena_off[c];
         double* __restrict__ Fp = F;
+        // fast-path children keep the CB rows of their delayed columns in W21 (upper part)
+        const bool wup = P.flag[(size_t)sh * P.nf + c] == FL_OK && ndo > 0;
         const int32_t* __restrict__ rm = P.rmap + P.rmap_ptr[c];
         const int dof = p + off;
         off += ndo > 0 ? ndo : 0;
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_beg
                         const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
                         if (lo >= clo && lo < chi) {
                             dst[u] = hi + (size_t)lo * ld;
-                            v[u] = colc[i];
+                            v[u] = (wup && j < ndo && i >= ndo) ? Fc[(ec + j) + (size_t)(ec + i) * fc] : colc[i];
                         }
                     }
                 }

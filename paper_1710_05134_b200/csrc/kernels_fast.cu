@@ -38,12 +38,11 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restrict__ items) {
-    // A operand: W21 rows with one halo column each side (2x2 partners),
-    // turned into L21 = W21 D^-1 in shared memory; B operand: W21 rows.
-    __shared__ __align__(16) double Aw[2][KC + 2][APAD];
+    // CB -= L21 D L21^T = G S G^T: both operands are rows of G (upper part, written by
+    // k_l21), S = diag(+-1) applied to the B fragments as sign-bit flips (no FP64 work).
+    __shared__ __align__(16) double As[2][KC][APAD];
     __shared__ __align__(16) double Bs[2][ST][BPAD];
-    __shared__ double Ga[2][KC], Gb[2][KC];             // L[:, t] = W[:, t] Ga[t] + W[:, t + Go[t]] Gb[t]
-    __shared__ int Go[2][KC];
+    __shared__ unsigned long long Sg[2][KC];
     const int4 it = items[blockIdx.x];          // (front, I, J, -)
     const int s = it.x, I = it.y, J = it.z;
     const int sh = blockIdx.y;
@@ -62,29 +61,18 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
     const int g = lane >> 2, tg = lane & 3;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
     auto load = [&](int buf, int t0) {
-        for (int x = tid; x < (KC + 2) * ST; x += SCH_T) {
-            const int i = x / (KC + 2), tt = x - i * (KC + 2);
-            const int gi = r0 + i, gt = t0 - 1 + tt;
-            const bool v = gi < f && gt >= 0 && gt < e;
-            cp_async8(&Aw[buf][tt][i], F + (v ? (gt + (size_t)gi * ld) : 0), v);
+        for (int x = tid; x < KC * ST; x += SCH_T) {
+            const int i = x / KC, tt = x - i * KC;
+            const int gi = r0 + i, gt = t0 + tt;
+            const bool v = gi < f && gt < e;
+            cp_async8(&As[buf][tt][i], F + (v ? (gt + (size_t)gi * ld) : 0), v);
         }
+        if (tid < KC) Sg[buf][tid] = (t0 + tid < e && A.sgn[t0 + tid] < 0.0) ? 0x8000000000000000ull : 0ull;
         for (int x = tid; x < KC * ST; x += SCH_T) {
             const int jj = x / KC, t = x % KC;
             const int gj = c0 + jj, gt = t0 + t;
             const bool v = gj < f && gt < e;
             cp_async8(&Bs[buf][jj][t], F + (v ? (gt + (size_t)gj * ld) : 0), v);
-        }
-        if (tid < KC) {
-            const int t = t0 + tid;
-            double ga = 0.0, gb = 0.0;
-            int o = 0;
-            if (t < e) {
-                const int kd = A.kind[t];
-                ga = A.fa[t];
-                gb = A.fb[t];
-                o = kd == PK_2X2A ? 1 : (kd == PK_2X2B ? -1 : 0);
-            }
-            Ga[buf][tid] = ga; Gb[buf][tid] = gb; Go[buf][tid] = o;
         }
         cp_async_commit();
     };
@@ -107,14 +95,11 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
 #pragma unroll
         for (int k4 = 0; k4 < KC; k4 += 4) {
             double a[4], b[4];
-            const int tt = k4 + tg;
-            const double ga = Ga[buf][tt], gb = Gb[buf][tt];
-            const double* w0 = &Aw[buf][tt + 1][wm + g];
-            const double* w1 = &Aw[buf][tt + 1 + Go[buf][tt]][wm + g];
 #pragma unroll
-            for (int mb = 0; mb < 4; ++mb) a[mb] = fma(w0[8 * mb], ga, w1[8 * mb] * gb);   // L21 = W21 D^-1
+            for (int mb = 0; mb < 4; ++mb) a[mb] = As[buf][k4 + tg][wm + 8 * mb + g];
 #pragma unroll
-            for (int nb = 0; nb < 4; ++nb) b[nb] = Bs[buf][wn + 8 * nb + g][k4 + tg];
+            for (int nb = 0; nb < 4; ++nb)
+                b[nb] = __longlong_as_double(__double_as_longlong(Bs[buf][wn + 8 * nb + g][k4 + tg]) ^ (long long)Sg[buf][k4 + tg]);
 #pragma unroll
             for (int mb = 0; mb < 4; ++mb)
 #pragma unroll

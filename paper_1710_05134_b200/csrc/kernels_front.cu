@@ -52,6 +52,8 @@ constexpr int FT = 256;                         // k_fs / k_check threads
 constexpr int LT = 256;                         // k_l21 threads (8 warps x 16 rows)
 constexpr int LR = 128;                         // k_l21 CB rows per CTA
 constexpr int LB = 32;                          // k_l21 column block
+constexpr int LST = 3;                          // k_l21 cp.async pipeline depth
+static_assert(LT == 8 * LB, "k_l21 column-max reduction maps 8 threads to a column");
 constexpr int KC = 16;                          // K chunk of the k_l21 GEMM
 constexpr int APAD = LR + 4;                    // = 4 (mod 16): conflict-free f64 fragments
 constexpr int BP = KC + 4;
@@ -468,6 +470,26 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
                 A.fb[cpos] = S.fb[t];
                 A.kind[cpos] = S.tp[t];
                 A.step[cpos] = S.st[t];
+                if (o == 0) {                                       // 1x1 (or zero): G = W sign(d) / sqrt|d|
+                    const double dd = S.d1[t], sg = dd < 0.0 ? -1.0 : 1.0;
+                    A.sgn[cpos] = sg;
+                    A.gca[cpos] = S.tp[t] == PK_ZERO ? 0.0 : sg / sqrt(fabs(dd));
+                    A.gcb[cpos] = 0.0;
+                    A.hca[cpos] = S.tp[t] == PK_ZERO ? 0.0 : sg * sqrt(fabs(dd));   // d / sqrt|d|
+                    A.hcb[cpos] = 0.0;
+                } else if (o == 1) {                                // 2x2: G = W Q |Lambda|^-1/2 S
+                    double cs, sn, l1, l2;
+                    pair_eig(S.d1[t], S.d2[t], S.d1[t + 1], cs, sn, l1, l2);
+                    const double s1 = l1 < 0.0 ? -1.0 : 1.0, s2 = l2 < 0.0 ? -1.0 : 1.0;
+                    const double k1 = s1 / sqrt(fabs(l1)), k2 = s2 / sqrt(fabs(l2));
+                    A.sgn[cpos] = s1;
+                    A.sgn[cpos + 1] = s2;
+                    A.gca[cpos] = cs * k1;      A.gcb[cpos] = sn * k1;        // G_t   = (W_t cs + W_t+1 sn) k1
+                    A.gca[cpos + 1] = cs * k2;  A.gcb[cpos + 1] = -sn * k2;   // G_t+1 = (W_t+1 cs - W_t sn) k2
+                    const double h1 = s1 * sqrt(fabs(l1)), h2 = s2 * sqrt(fabs(l2));   // D M^-T = Q S |Lambda|^1/2
+                    A.hca[cpos] = cs * h1;      A.hcb[cpos] = sn * h1;        // B'_t   = L_t cs h1 + L_t+1 sn h1
+                    A.hca[cpos + 1] = cs * h2;  A.hcb[cpos + 1] = -sn * h2;   // B'_t+1 = L_t+1 cs h2 - L_t sn h2
+                }
             }
         }
         __syncthreads();
@@ -553,20 +575,55 @@ __global__ void __launch_bounds__(UT) k_fsu(DevPlan P, const int4* __restrict__ 
             }
 }
 
+// ------------------------------------------------------------------ k_prep
+// After the FS factorisation of a front: L11 -> B' = L11 D M^-T in place (rows below
+// each pivot block), so that W21 L11^T = G B'^T with G = W21 D^-1 M (k_l21, k_schur).
+__global__ void __launch_bounds__(FT) k_prep(DevPlan P, const int32_t* __restrict__ fronts) {
+    const int s = fronts[blockIdx.x];
+    const int sh = blockIdx.y;
+    if (P.flag[(size_t)sh * P.nf + s] != FL_ACTIVE) return;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int q = p + nd, ld = P.forder[s] + nd;
+    const int e = q - P.nd_out[(size_t)sh * P.nf + s];
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < e; t += FT / 32) {
+        const int kd = A.kind[t];
+        if (kd == PK_2X2B) continue;                    // handled with its first column
+        double* c0 = F + (size_t)t * ld;
+        if (kd == PK_2X2A) {
+            double* c1 = c0 + ld;
+            const double a0 = A.hca[t], b0 = A.hcb[t], a1 = A.hca[t + 1], b1 = A.hcb[t + 1];
+            for (int j = t + 2 + lane; j < q; j += 32) {
+                const double l0 = c0[j], l1 = c1[j];
+                c0[j] = l0 * a0 + l1 * b0;
+                c1[j] = l1 * a1 + l0 * b1;
+            }
+        } else {
+            const double a0 = A.hca[t];
+            for (int j = t + 1 + lane; j < q; j += 32) c0[j] *= a0;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ k_l21
 // W21 = A21 P^T L11^-T for 64 CB rows of one front; column maxima of W21.
 // L11[i,t] = 0 for t >= e (delayed columns have no pivot: their W21 column
 // is the fully updated CB part of the delayed column).
 __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict__ items) {
     extern __shared__ __align__(16) double l21_smem[];
-    double (*As)[KC][APAD] = reinterpret_cast<double (*)[KC][APAD]>(l21_smem);                  // [2][KC][APAD]
-    double (*Bs)[LB][BP] = reinterpret_cast<double (*)[LB][BP]>(l21_smem + 2 * KC * APAD);      // [2][LB][BP]
-    double (*Sbase)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + 2 * KC * APAD + 2 * LB * BP);
-    static_assert(LR * (LB + 1) <= 2 * KC * APAD, "Sacc aliases As");
-    static_assert(LB * (LB + 1) <= 2 * LB * BP, "Lbb aliases Bs");
+    double (*As)[KC][APAD] = reinterpret_cast<double (*)[KC][APAD]>(l21_smem);                   // [LST][KC][APAD]
+    double (*Bs)[LB][BP] = reinterpret_cast<double (*)[LB][BP]>(l21_smem + LST * KC * APAD);      // [LST][LB][BP]
+    double (*Sbase)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * KC * APAD + LST * LB * BP);
+    static_assert(LR * (LB + 1) <= LST * KC * APAD, "Sacc aliases As");
+    static_assert(LB * (LB + 1) <= LST * LB * BP, "Lbb aliases Bs");
     double (*Sacc)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem);
-    double (*Lbb)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + 2 * KC * APAD);
+    double (*Lbb)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * KC * APAD);
     __shared__ int sperm[LB];
+    __shared__ int skind[LB];                             // pivot kind of the block columns (-1: delayed / none)
+    __shared__ double sgca[LB], sgcb[LB];
     const int4 it = items[blockIdx.x];
     const int s = it.x, I = it.y;
     const int sh = blockIdx.y;
@@ -587,10 +644,18 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
     const int g = lane >> 2, tg = lane & 3;
     const int wm = warp * 16;
     const int row = tid >> 1, half = tid & 1;               // triangle: two threads per CB row
-    for (int b0 = 0; b0 < q; b0 += LB) {
-        const int nbc = min(LB, q - b0);
+    for (int b0 = 0, nbc = 0; b0 < q; b0 += nbc) {
+        nbc = min(LB, q - b0);
+        if (nbc == LB && b0 + LB - 1 < e && A.kind[b0 + LB - 1] == PK_2X2A) nbc = LB - 1;   // keep 2x2 pairs whole
         const int K = min(b0, e);
-        if (tid < LB) sperm[tid] = tid < nbc ? A.perm[b0 + tid] : 0;
+        if (tid < LB) {
+            const int t = b0 + tid;
+            sperm[tid] = tid < nbc ? A.perm[t] : 0;
+            const bool el = tid < nbc && t < e;
+            skind[tid] = el ? A.kind[t] : -1;
+            sgca[tid] = el ? A.gca[t] : 0.0;
+            sgcb[tid] = el ? A.gcb[t] : 0.0;
+        }
         __syncthreads();
         // gathered A21 columns of the block (A21 P^T), fetched while the GEMM runs
         for (int x = tid; x < LB * LR; x += LT) {
@@ -622,16 +687,20 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
                 cp_async_commit();
             };
             const int nk = (K + KC - 1) / KC;
-            load(0, 0);
+#pragma unroll
+            for (int st0 = 0; st0 < LST - 1; ++st0) {
+                if (st0 < nk) load(st0, st0 * KC);
+                else cp_async_commit();
+            }
             for (int kc = 0; kc < nk; ++kc) {
-                const int buf = kc & 1;
-                if (kc + 1 < nk) {
-                    load(buf ^ 1, (kc + 1) * KC);
-                    cp_async_wait<1>();
-                } else {
-                    cp_async_wait<0>();
+                const int buf = kc % LST;
+                cp_async_wait<LST - 2>();
+                __syncthreads();                    // chunk kc landed (and the gathered columns)
+                {
+                    const int nx = kc + LST - 1;
+                    if (nx < nk) load(nx % LST, nx * KC);
+                    else cp_async_commit();
                 }
-                __syncthreads();
 #pragma unroll
                 for (int k4 = 0; k4 < KC; k4 += 4) {
                     double a[2], b[4];
@@ -644,8 +713,9 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
 #pragma unroll
                         for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb], a[mb], b[nb]);
                 }
-                __syncthreads();
             }
+            cp_async_wait<0>();
+            __syncthreads();                        // all chunks consumed before Sacc aliases As
         } else {
             cp_async_wait<0>();
             __syncthreads();
@@ -656,7 +726,7 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
             for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) Sacc[wm + 8 * mb + g][8 * nb + 2 * tg + h] = acc[mb][nb][h];
-        // diagonal block of L11 (strict lower, columns < e only)
+        // diagonal block of B' = L11 D M^-T (strict lower, columns < e only; k_prep)
         for (int x = tid; x < LB * LB; x += LT) {
             const int a = x / LB, b = x - a * LB;
             double v = 0.0;
@@ -664,39 +734,57 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
             Lbb[a][b] = v;
         }
         __syncthreads();
-        {   // in-block unit-lower solve: thread pair (row, parity) splits each dot product
+        {   // in-block solve in G space: x_t = A_t - sum_{t' < t} G_t' B'[t, t'] (G of the block's earlier
+            // columns; a 2x2 pair's G is formed when its second column is known).  Thread pair
+            // (row, parity) splits each dot product.
             const int i = r0 + row;
             const bool valid = i < f;
-            double xh[LB / 2];
+            double gh[LB / 2], ah[LB / 2];                   // own-parity columns: G (raw for delayed), |W21|
+            double vprev = 0.0;
 #pragma unroll
             for (int t = 0; t < LB; ++t) {
                 double p0 = 0.0, p1 = 0.0;
 #pragma unroll
                 for (int u = 0; 2 * u + half < t && u < LB / 2; u += 2) {
-                    p0 = fma(xh[u], Lbb[t][2 * u + half], p0);
-                    if (2 * (u + 1) + half < t) p1 = fma(xh[u + 1], Lbb[t][2 * (u + 1) + half], p1);
+                    p0 = fma(gh[u], Lbb[t][2 * u + half], p0);
+                    if (2 * (u + 1) + half < t) p1 = fma(gh[u + 1], Lbb[t][2 * (u + 1) + half], p1);
                 }
                 const double part = p0 + p1;
                 const double tot = part + __shfl_xor_sync(0xffffffffu, part, 1);
                 double v = Sbase[row][t] - Sacc[row][t] - tot;
                 v = (t < nbc && valid) ? v : 0.0;
-                if ((t & 1) == half) xh[t >> 1] = v;
+                const int kd = skind[t];
+                const bool own = (t & 1) == half;
+                if (own) { ah[t >> 1] = fabs(v); gh[t >> 1] = v; }
+                if (kd == PK_1X1 || kd == PK_ZERO) {
+                    if (own) gh[t >> 1] = v * sgca[t];
+                } else if (kd == PK_2X2B && t > 0) {
+                    if (own) gh[t >> 1] = v * sgca[t] + vprev * sgcb[t];
+                    else gh[(t - 1) >> 1] = vprev * sgca[t - 1] + v * sgcb[t - 1];
+                }
+                vprev = v;
             }
             if (valid) {
                 double* __restrict__ Wi = F + (size_t)i * ld + b0;
 #pragma unroll
                 for (int u = 0; u < LB / 2; ++u)
-                    if (2 * u + half < nbc) Wi[2 * u + half] = xh[u];
+                    if (2 * u + half < nbc) Wi[2 * u + half] = gh[u];
             }
+            __syncwarp();                                    // both threads of the row are done with Sbase
 #pragma unroll
-            for (int t = 0; t < LB; ++t) {
-                if (t < nbc && b0 + t < e) {
-                    double m = ((t & 1) == half) ? fabs(xh[t >> 1]) : 0.0;
+            for (int u = 0; u < LB / 2; ++u) Sbase[row][2 * u + half] = valid ? ah[u] : 0.0;
+        }
+        __syncthreads();
+        {   // CB column maxima of W21 (threshold tests, k_check): 8 threads per column, 16 rows each
+            const int t = tid >> 3, part = tid & 7;
+            double m = 0.0;
 #pragma unroll
-                    for (int o2 = 16; o2 > 0; o2 >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o2));
-                    if (lane == 0 && m > 0.0) atomicMax(&A.cm[b0 + t], (unsigned long long)__double_as_longlong(m));
-                }
-            }
+            for (int r = 0; r < LR / 8; ++r) m = fmax(m, Sbase[part * (LR / 8) + r][t]);
+            m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+            m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+            m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 4));
+            if (part == 0 && t < nbc && b0 + t < e && m > 0.0)
+                atomicMax(&A.cm[b0 + t], (unsigned long long)__double_as_longlong(m));
         }
         __syncthreads();
     }
@@ -788,12 +876,7 @@ __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restri
     }
     __syncthreads();
     if (!s_ok) {
-        // restore the assembled FS block; the unblocked kernel redoes this front
-        const int warp = tid >> 5, lane = tid & 31;
-        for (int j = warp; j < q; j += FT / 32) {
-            for (int i = j + 1 + lane; i < q; i += 32) F[i + (size_t)j * ld] = F[j + (size_t)i * ld];
-            if (lane == 0) F[j + (size_t)j * ld] = A.diag[j];
-        }
+        // the restores (k_restore21, k_restore11) run next; then a rerun or the unblocked kernel
         if (tid == 0) {
             int32_t* forced = P.forced + ((size_t)sh * P.nf + s) * (FMAX + 1);
             const int nf_ = forced[0];
@@ -810,28 +893,24 @@ __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restri
         return;
     }
     if (tid == 0) *flag = FL_OK;
-    // D^-1 coefficients for k_schur (L21 = W21 D^-1 there), into the fa / fb slots:
-    // L[:, t] = W[:, t] * fa[t] + W[:, partner] * fb[t]
-    for (int t = tid; t < e; t += FT) {
-        const int kd = A.kind[t];
-        double ga = 0.0, gb = 0.0;
-        if (kd == PK_1X1) ga = 1.0 / A.d[t];
-        else if (kd == PK_2X2A || kd == PK_2X2B) {
-            const int a = kd == PK_2X2A ? t : t - 1;
-            const double d11 = A.d[a], d21 = A.ds[a], d22 = A.d[a + 1];
-            const double det = d11 * d22 - d21 * d21;
-            ga = (kd == PK_2X2A ? d22 : d11) / det;
-            gb = -d21 / det;
-        }
-        A.fa[t] = ga;
-        A.fb[t] = gb;
-    }
-    if (root || e == q) return;
-    // delayed columns [e, q): their updated CB rows (upper W21) to the lower part,
-    // where the parent's extend-add reads them
-    for (int idx = tid; idx < (q - e) * c; idx += FT) {
-        const int t = e + idx / c, i = q + idx % c;
-        F[i + (size_t)t * ld] = F[t + (size_t)i * ld];
+}
+
+// ------------------------------------------------------------------ restore of a failed front
+// the assembled FS block from its transposed copy in the upper triangle
+__global__ void __launch_bounds__(FT) k_restore11(DevPlan P, const int32_t* __restrict__ fronts) {
+    const int s = fronts[blockIdx.x];
+    const int sh = blockIdx.y;
+    const int fl = P.flag[(size_t)sh * P.nf + s];
+    if (fl != FL_RERUN && fl != FL_REF) return;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int q = p + nd, ld = P.forder[s] + nd;
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = warp; j < q; j += FT / 32) {
+        for (int i = j + 1 + lane; i < q; i += 32) F[i + (size_t)j * ld] = F[j + (size_t)i * ld];
+        if (lane == 0) F[j + (size_t)j * ld] = A.diag[j];
     }
 }
 
@@ -887,9 +966,14 @@ void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cuda
     k_fsu<<<dim3(nitems, batch), UT, 0, st>>>(P, items);
 }
 
+void launch_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    k_prep<<<dim3(nfronts, batch), FT, 0, st>>>(P, fronts);
+}
+
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
     if (nitems <= 0) return;
-    const size_t smem = sizeof(double) * (2 * KC * APAD + 2 * LB * BP + LR * (LB + 1));
+    const size_t smem = sizeof(double) * (LST * KC * APAD + LST * LB * BP + LR * (LB + 1));
     static bool attr = false;
     if (!attr) { cudaFuncSetAttribute(k_l21, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
     k_l21<<<dim3(nitems, batch), LT, smem, st>>>(P, items);
@@ -898,6 +982,13 @@ void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cuda
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
     if (nfronts <= 0) return;
     k_check<<<dim3(nfronts, batch), FT, 0, st>>>(P, fronts);
+}
+
+void launch_restore(const DevPlan& P, const int32_t* fronts, int nfronts, const int4* litems, int nlitems, int batch,
+                    cudaStream_t st) {
+    (void)litems;
+    (void)nlitems;                       // A21 is never overwritten: the FS block is all there is to restore
+    if (nfronts > 0) k_restore11<<<dim3(nfronts, batch), FT, 0, st>>>(P, fronts);
 }
 
 }  // namespace kep

@@ -36,8 +36,8 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 // Copy the factor panel of each front of a level (shift 0 of the batch) into
-// the factor store.  Fast-path fronts keep W21 in the upper part: L21 = W21 D^-1
-// (coefficients left in fa / fb by k_check); unblocked fronts keep L in the lower part.
+// the factor store.  Fast-path fronts keep G = L21 Q |Lambda|^1/2 in the upper part
+// (k_l21); unblocked fronts keep L in the lower part in position order.
 __global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const int32_t* __restrict__ fronts) {
     const int s = fronts[blockIdx.x];
     const int nd = P.nd_in[s];
@@ -60,13 +60,28 @@ __global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const in
     }
     for (int t = 0; t < e; ++t) {
         const int kd = A.kind[t];
-        const int o = kd == PK_2X2A ? 1 : (kd == PK_2X2B ? -1 : 0);
+        // fast path, CB rows: L21 = G M^-1 (G = L21 Q |Lambda|^1/2 in the upper part, k_l21)
+        double ca = 0.0, cb = 0.0;
+        int o = 0;
+        if (kd == PK_1X1) ca = 1.0 / sqrt(fabs(A.d[t]));
+        else if (kd == PK_2X2A || kd == PK_2X2B) {
+            const int a = kd == PK_2X2A ? t : t - 1;
+            double cs, sn, l1, l2;
+            pair_eig(A.d[a], A.ds[a], A.d[a + 1], cs, sn, l1, l2);
+            const double r1 = 1.0 / sqrt(fabs(l1)), r2 = 1.0 / sqrt(fabs(l2));
+            if (kd == PK_2X2A) { ca = cs * r1; cb = -sn * r2; o = 1; }    // L_t = cs G_t/r1' - sn G_t+1/r2'
+            else { ca = cs * r2; cb = sn * r1; o = -1; }                  // L_t+1 = sn G_t/r1' + cs G_t+1/r2'
+        }
         double* col = panel + (size_t)t * ld;
         for (int i = threadIdx.x; i < f; i += ST_T) {
             double v = 0.0;
             if (i > t && !(kd == PK_2X2A && i == t + 1)) {
-                if (i < q || flag == FL_REF) v = F[i + (size_t)t * ld];
-                else v = F[t + (size_t)i * ld] * A.fa[t] + (o ? F[(t + o) + (size_t)i * ld] * A.fb[t] : 0.0);
+                if (flag == FL_REF) v = F[i + (size_t)t * ld];
+                else if (i < q) {      // fast path FS rows hold B' = L11 D M^-T (k_prep): L11 = B' (D M^-T)^-1
+                    if (kd == PK_2X2A) v = F[i + (size_t)t * ld] * A.gca[t] + F[i + (size_t)(t + 1) * ld] * A.gcb[t + 1];
+                    else if (kd == PK_2X2B) v = F[i + (size_t)t * ld] * A.gca[t] + F[i + (size_t)(t - 1) * ld] * A.gcb[t - 1];
+                    else v = F[i + (size_t)t * ld] * A.gca[t];
+                } else v = F[t + (size_t)i * ld] * ca + (o ? F[(t + o) + (size_t)i * ld] * cb : 0.0);
             }
             if (kd == PK_ZERO) v = 0.0;
             col[i] = v;

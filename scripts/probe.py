@@ -14,12 +14,13 @@ def run(p, nshift, variant=0, batch=16):
     nus, st = k.inertia_many(sig[:2])       # warm
     torch.cuda.synchronize()
     k.reset_profile()
-    t = time.time(); nus, st = k.inertia_many(sig); dt = time.time() - t
+    t = time.time(); nus, st, infos = k.inertia_many(sig, with_info=True); dt = time.time() - t
     prof = k.profile()
     a = k.analysis()
     print(json.dumps(dict(name=p.name, n=p.n, analyze_s=ta, bounds_s=tb, shifts=nshift, s_per_shift=dt / nshift,
                           shifts_per_s=nshift / dt, gflops=a["flops"] * nshift / dt / 1e9, nus=nus.tolist()[:8],
-                          st=st.tolist()[:8], sigma=sig.tolist()[:8], profile=prof, analysis=a)), flush=True)
+                          st=st.tolist()[:8], sigma=sig.tolist()[:8], profile=prof, analysis=a, redo_per_shift=sum(i.n_redo for i in infos) / nshift,
+                          delayed_per_shift=sum(i.n_delayed for i in infos) / nshift, n2x2_per_shift=sum(i.n_2x2 for i in infos) / nshift)), flush=True)
 
 which = sys.argv[1:] or ["c1", "c2"]
 for w in which:
