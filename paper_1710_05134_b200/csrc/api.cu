@@ -447,7 +447,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
         for (int L = 0; L < nl; ++L) {
             const int b = S.level_ptr[L], nfl = S.level_ptr[L + 1] - b;
             mark(KEP_K_ASSEMBLE, true);
-            kep::launch_assemble(P, b, nfl, m, c->stream);
+            kep::launch_assemble(P, c->d_level_fronts + b, nfl, m, false, c->stream);
             mark(KEP_K_ASSEMBLE, false);
             c->prof.launches[KEP_K_ASSEMBLE]++;
             if (c->fast_cnt[L]) {
@@ -488,7 +488,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                     }
                     mark(KEP_K_CHECK, true);
                     kep::launch_check(P, fl, nfl2, m, c->stream);
-                    kep::launch_restore(P, fl, nfl2, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, c->stream);
+                    kep::launch_assemble(P, fl, nfl2, m, true, c->stream);   // restore failed fronts: assemble again
                     mark(KEP_K_CHECK, false);
                     c->prof.launches[KEP_K_CHECK] += 3;
                 }

@@ -131,7 +131,8 @@ struct StorePlan {
 };
 
 // Launchers (kernels.cu, kernels_front.cu, kernels_fast.cu, kernels_solve.cu)
-void launch_assemble(const DevPlan& P, int lvl_begin, int nfronts, int batch, cudaStream_t st);
+void launch_assemble(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, bool only_flagged,
+                     cudaStream_t st);
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st);
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 int fs_iters(int qmax);               // k_fsp launches that finish every front of a level
@@ -150,8 +151,6 @@ void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const dou
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 void launch_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
-void launch_restore(const DevPlan& P, const int32_t* fronts, int nfronts, const int4* litems, int nlitems, int batch,
-                    cudaStream_t st);
 int front_nb_for(int qmax);           // block width for a level (0: too large, use the reference kernel)
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,

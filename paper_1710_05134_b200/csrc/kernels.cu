@@ -114,10 +114,15 @@ __device__ __forceinline__ void tri_split(int ld, int S, int x, int& lo, int& hi
 // owns the parent columns [lo, hi): zero-fill, original entries (alpha a - sigma b),
 // then the children's CB entries landing in those columns, children in order.
 // Each parent entry belongs to one CTA, so the sum order is fixed (deterministic).
-__global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, int lvl_begin, int S) {
-    const int s = P.level_fronts[lvl_begin + blockIdx.x / S];
+__global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32_t* __restrict__ list, int S,
+                                                          int only_flagged) {
+    const int s = list[blockIdx.x / S];
     const int xs = blockIdx.x % S;
     const int sh = blockIdx.y;
+    if (only_flagged) {               // re-assembly of fronts whose fast-path pass failed (restore)
+        const int fl = P.flag[(size_t)sh * P.nf + s];
+        if (fl != FL_RERUN && fl != FL_REF) return;
+    }
     ShiftStat* st = P.stats + sh;
     double* arena = P.arena + (size_t)sh * P.arena_stride;
     int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
@@ -459,11 +464,13 @@ __global__ void k_reset_stats(ShiftStat* st, int batch) {
 
 }  // namespace
 
-void launch_assemble(const DevPlan& P, int lvl_begin, int nfronts, int batch, cudaStream_t st) {
+void launch_assemble(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, bool only_flagged,
+                     cudaStream_t st) {
+    if (nfronts <= 0) return;
     // CTAs per front: enough to give ~4 resident CTAs per SM on the whole level
     int S = (int)((4 * 148 + (int64_t)nfronts * batch - 1) / ((int64_t)nfronts * batch));
     S = std::max(1, std::min(S, 16));
-    k_assemble<<<dim3(nfronts * S, batch), kAsmThreads, 0, st>>>(P, lvl_begin, S);
+    k_assemble<<<dim3(nfronts * S, batch), kAsmThreads, 0, st>>>(P, fronts, S, only_flagged ? 1 : 0);
 }
 
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,

@@ -20,9 +20,8 @@
 //          choice (alpha = (1+sqrt17)/8) among the FS candidates, threshold
 //          test with the FS maxima (a column failing there is delayed — the
 //          full test fails too), rank-nb DMMA update of the FS trailing
-//          block.  The assembled A11 is kept (transposed) in the free upper
-//          triangle so the front can be restored.  Records, per position,
-//          the pivot kind, D, the FS maxima and the permutation.
+//          block (k_fsu).  Records, per position, the pivot kind, D, the FS
+//          maxima and the permutation.
 //  k_l21   many CTAs per front: 64 CB rows each, the unit-triangular solve
 //          W21 = A21 P^T L11^-T (DMMA for the off-block part), written to
 //          the upper triangle of the CB columns, and the column maxima of
@@ -30,8 +29,9 @@
 //  k_check one CTA per front: re-evaluates every test in pivot order with
 //          the full-column maxima.  All pass -> the pivot sequence is the
 //          unblocked rule's; inertia is counted and L21 = W21 D^-1 written.
-//          A failure -> the front is restored to its assembled state and
-//          flagged; k_factor_ref (the unblocked rule itself) redoes it.
+//          A failure -> the front is assembled again (its children's CBs are
+//          still live during the level) and rerun with a forced delay at the
+//          failing step, or after FMAX reruns handed to k_factor_ref.
 //
 // Storage per front (column-major, ld = f):  L[i,t] at F[i + t*ld] (i > t;
 // 0 at the subdiagonal of a 2x2 block, whose D lives in the aux record),
@@ -290,13 +290,6 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
     int e = 0, qe = q;
     int step = 0, fnext = 0;                           // S1 actions so far; next forced delay
     if (mode < 2) {
-        // keep the assembled A11 (strict lower -> upper, diagonal -> aux) for a restore
-        if (!root) {
-            for (int j = warp; j < q; j += TH / 32) {
-                for (int i = j + 1 + lane; i < q; i += 32) F[j + (size_t)i * ld] = F[i + (size_t)j * ld];
-                if (lane == 0) A.diag[j] = F[j + (size_t)j * ld];
-            }
-        }
         for (int i = tid; i < q; i += TH) { A.perm[i] = i; A.cm[i] = 0ull; }
     } else {
         e = fst[0]; qe = fst[1]; step = fst[2]; fnext = fst[3];
@@ -876,7 +869,7 @@ __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restri
     }
     __syncthreads();
     if (!s_ok) {
-        // the restores (k_restore21, k_restore11) run next; then a rerun or the unblocked kernel
+        // the front is assembled again next (k_assemble, flagged mode); then a rerun or the unblocked kernel
         if (tid == 0) {
             int32_t* forced = P.forced + ((size_t)sh * P.nf + s) * (FMAX + 1);
             const int nf_ = forced[0];
@@ -893,25 +886,6 @@ __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restri
         return;
     }
     if (tid == 0) *flag = FL_OK;
-}
-
-// ------------------------------------------------------------------ restore of a failed front
-// the assembled FS block from its transposed copy in the upper triangle
-__global__ void __launch_bounds__(FT) k_restore11(DevPlan P, const int32_t* __restrict__ fronts) {
-    const int s = fronts[blockIdx.x];
-    const int sh = blockIdx.y;
-    const int fl = P.flag[(size_t)sh * P.nf + s];
-    if (fl != FL_RERUN && fl != FL_REF) return;
-    const int nd = P.nd_in[(size_t)sh * P.nf + s];
-    const int p = P.npiv[s], c = P.ncb[s];
-    const int q = p + nd, ld = P.forder[s] + nd;
-    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
-    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = warp; j < q; j += FT / 32) {
-        for (int i = j + 1 + lane; i < q; i += 32) F[i + (size_t)j * ld] = F[j + (size_t)i * ld];
-        if (lane == 0) F[j + (size_t)j * ld] = A.diag[j];
-    }
 }
 
 }  // namespace
@@ -984,11 +958,5 @@ void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batc
     k_check<<<dim3(nfronts, batch), FT, 0, st>>>(P, fronts);
 }
 
-void launch_restore(const DevPlan& P, const int32_t* fronts, int nfronts, const int4* litems, int nlitems, int batch,
-                    cudaStream_t st) {
-    (void)litems;
-    (void)nlitems;                       // A21 is never overwritten: the FS block is all there is to restore
-    if (nfronts > 0) k_restore11<<<dim3(nfronts, batch), FT, 0, st>>>(P, fronts);
-}
 
 }  // namespace kep
