@@ -73,9 +73,13 @@ struct Red {
     double x[3][8];
 };
 
-// block-wide (max, argmax) of a and max of b, c, d
+// block-wide (max, argmax) of a and max of b, c, d.  R points at two scratch
+// records used alternately (flip toggles), so one barrier per reduction suffices:
+// a record is rewritten two reductions later, after another barrier.
 template <int TH>
-__device__ void block_reduce(MaxIdx& a, double& b, double& c, double& d, Red* R) {
+__device__ void block_reduce(MaxIdx& a, double& b, double& c, double& d, Red* R2, int& flip) {
+    Red* R = R2 + flip;
+    flip ^= 1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         MaxIdx y;
@@ -87,7 +91,6 @@ __device__ void block_reduce(MaxIdx& a, double& b, double& c, double& d, Red* R)
         d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
     }
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
     if (l == 0) { R->mi[w] = a; R->x[0][w] = b; R->x[1][w] = c; R->x[2][w] = d; }
     __syncthreads();
     a = R->mi[0]; b = R->x[0][0]; c = R->x[1][0]; d = R->x[2][0];
@@ -176,7 +179,7 @@ __device__ Smem<NB> carve(double* base, int RS) {
     S.d2 = p; p += NB;
     S.fa = p; p += NB;
     S.fb = p; p += NB;
-    S.red = (Red*)p; p += (sizeof(Red) + 7) / 8;
+    S.red = (Red*)p; p += (2 * sizeof(Red) + 7) / 8;
     S.oo = (int*)p; p += (NB + 1) / 2;
     S.tp = (int*)p; p += (NB + 1) / 2;
     S.st = (int*)p; p += (NB + 1) / 2;
@@ -187,7 +190,7 @@ __device__ Smem<NB> carve(double* base, int RS) {
 }  // namespace
 
 size_t fs_smem_bytes(int nb, int RS) {
-    size_t d = (size_t)nb * RS + 2 * (size_t)RS + 8 * nb + (sizeof(Red) + 7) / 8 + 3 * ((nb + 1) / 2) + (RS + 1) / 2;
+    size_t d = (size_t)nb * RS + 2 * (size_t)RS + 8 * nb + (2 * sizeof(Red) + 7) / 8 + 3 * ((nb + 1) / 2) + (RS + 1) / 2;
     return d * sizeof(double);
 }
 
@@ -289,6 +292,7 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
 
     int e = 0, qe = q;
     int step = 0, fnext = 0;                           // S1 actions so far; next forced delay
+    int rflip = 0;                                     // block_reduce scratch toggle
     if (mode < 2) {
         for (int i = tid; i < q; i += TH) { A.perm[i] = i; A.cm[i] = 0ull; }
     } else {
@@ -333,7 +337,7 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
                     }
                 }
             }
-            block_reduce<TH>(mC, mR, z1, z2, S.red);
+            block_reduce<TH>(mC, mR, z1, z2, S.red, rflip);
             const double gC = mC.v > 0.0 ? mC.v : 0.0;
             const int r = mC.v >= 0.0 ? mC.i : k;
             const double akk = fabs(S.wk[k - kp]);
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
                         if (i != k) { ma = fmax(ma, a); m3 = fmax(m3, fabs(S.wk[ii])); }
                     }
                 }
-                block_reduce<TH>(dm, mc, ma, m3, S.red);
+                block_reduce<TH>(dm, mc, ma, m3, S.red, rflip);
                 const double rho = mc;                       // includes |a_kr| = gC
                 rall = ma;                                   // column r, rows not in {k, r}
                 gk = m3;                                     // column k, rows not in {k, r}
