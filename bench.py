@@ -97,6 +97,16 @@ def fp64_peak_tflops():
     return 2.0 * N ** 3 / best / 1e12
 
 
+def traffic_per_launch(path=os.path.join(ROOT, "profiles", "r1_schur_traffic.json")):
+    """DRAM bytes (read + write) per k_schur launch, from the committed ncu capture of this
+    bench command (scripts/ncu_traffic.py); None if absent."""
+    try:
+        with open(path) as fh:
+            return json.load(fh)["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------------------- CPU oracle leg
 def cpu_oracle_sample(cfg: int, seconds_hint: float = 20.0):
     """Time the oracle (O-sparse, as it stands) on a bounded sample of the workload.
@@ -351,7 +361,7 @@ def main():
                 "achieved": (prof["schur_flops"] / sch_t / 1e12) if sch_t > 0 else None,
                 "peak": peak, "unit": "TFLOP/s",
                 "frac": (prof["schur_flops"] / sch_t / 1e12 / peak) if sch_t > 0 and peak > 0 else None,
-                "traffic": None,
+                "traffic": traffic_per_launch(),
                 "peak_source": "cuBLAS DGEMM 8192^3 measured live in bench.py (MEASURED_PEAKS.json has no FP64 entry)",
                 "kernel_ms": ms, "kernel_launches": prof["launches"], "dominant_by_time": dom,
                 "schur_flops_alg": prof["schur_flops"]}
