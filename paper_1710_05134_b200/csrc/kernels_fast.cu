@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
             for (int h = 0; h < 2; ++h) {
                 const int i = r0 + wm + 8 * mb + g;
                 const int j = c0 + wn + 8 * nb + 2 * tg + h;
-                if (i < f && j < f && i >= j) F[i + (size_t)j * ld] -= acc[mb][nb][h];
+                if (i < f && j < f && i >= j) atomicAdd(&F[i + (size_t)j * ld], -acc[mb][nb][h]);   // one writer: RED, no load wait
             }
 }
 

@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(UT) k_fsu(DevPlan P, const int4* __restrict__ 
             for (int h = 0; h < 2; ++h) {
                 const int i = i0 + wm + 8 * mb + g;
                 const int j = j0 + wn + 8 * nb + 2 * tg + h;
-                if (i < q && j < q && i >= j) F[i + (size_t)j * ld] -= acc[mb][nb][h];
+                if (i < q && j < q && i >= j) atomicAdd(&F[i + (size_t)j * ld], -acc[mb][nb][h]);   // one writer: RED
             }
 }
 
