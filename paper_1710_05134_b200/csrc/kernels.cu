@@ -243,12 +243,11 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32
                         }
                     }
                 }
-                double old[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) old[u] = dst[u] != SIZE_MAX ? Fp[dst[u]] : 0.0;
+                // one writer per parent entry and child (children ordered by the barrier
+                // between them): fire-and-forget RED adds, no load latency
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (dst[u] != SIZE_MAX) Fp[dst[u]] = old[u] + v[u];
+                    if (dst[u] != SIZE_MAX) atomicAdd(&Fp[dst[u]], v[u]);
             }
         }
     }
