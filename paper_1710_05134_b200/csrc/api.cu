@@ -455,7 +455,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 const int nfl2 = (int)c->fast_cnt[L];
                 // pass 0, then kReruns passes over the fronts whose full-column test failed
                 // (each with one more forced delay), then the unblocked kernel for the rest
-                const int iters = kep::fs_iters(c->level_qmax[L]);
+                const int iters = kep::fs_iters(c->level_qmax[L], (int64_t)nfl2 * m);
                 for (int pass = 0; pass <= kReruns; ++pass) {
                     if (pass > 0) {                     // any front flagged for a rerun at this level?
                         int32_t pend = 0;

@@ -135,7 +135,7 @@ void launch_assemble(const DevPlan& P, const int32_t* fronts, int nfronts, int b
                      cudaStream_t st);
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st);
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
-int fs_iters(int qmax);               // k_fsp launches that finish every front of a level
+int fs_iters(int qmax, int64_t nblocks);   // k_fsp launches that finish every front of a level
 void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, cudaStream_t st);
 void launch_fwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
 void launch_bwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
@@ -151,7 +151,7 @@ void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const dou
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 void launch_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
-int front_nb_for(int qmax);           // block width for a level (0: too large, use the reference kernel)
+int front_nb_for(int qmax, int64_t nblocks = 0);   // block width (0: too large, use the reference kernel)
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,
                         bool only_flagged = false);

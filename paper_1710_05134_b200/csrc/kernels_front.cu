@@ -40,6 +40,7 @@
 #include <climits>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -724,8 +725,8 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
 #pragma unroll
                 for (int h = 0; h < 2; ++h) Sacc[wm + 8 * mb + g][8 * nb + 2 * tg + h] = acc[mb][nb][h];
         // diagonal block of B' = L11 D M^-T (strict lower, columns < e only; k_prep)
-        for (int x = tid; x < LB * LB; x += LT) {
-            const int a = x / LB, b = x - a * LB;
+        for (int x = tid; x < LB * LB; x += LT) {           // consecutive threads walk a column (coalesced)
+            const int b = x / LB, a = x - b * LB;
             double v = 0.0;
             if (a < nbc && b < a && b0 + b < e) v = F[(b0 + a) + (size_t)(b0 + b) * ld];
             Lbb[a][b] = v;
@@ -900,17 +901,20 @@ int fs_rows_pad(int qmax) { return ((qmax + 15) / 16) * 16 + 4; }
 
 // NB for a level whose fronts have at most qmax fully-summed columns (with
 // slack): the widest block whose shared memory fits; 0 = too large.
-int front_nb_for(int qmax) {
+int front_nb_for(int qmax, int64_t nblocks) {
     const int RS = fs_rows_pad(qmax);
     const size_t lim = kFsSmemLimit;
-    if (fs_smem_bytes(32, RS) <= lim && qmax <= 640) return 32;
+    // NB = 32 halves the k_fsu passes but its Ls block (q x 32) leaves one CTA per SM for q > 384:
+    // worth it only when the level is too small to fill the GPU anyway
+    const int q32 = nblocks < 4 * 148 ? 640 : 384;
+    if (fs_smem_bytes(32, RS) <= lim && qmax <= q32) return 32;
     if (fs_smem_bytes(16, RS) <= lim) return 16;
     if (fs_smem_bytes(8, RS) <= lim) return 8;
     return 0;
 }
 
-int fs_iters(int qmax) {
-    const int nb = front_nb_for(qmax);
+int fs_iters(int qmax, int64_t nblocks) {
+    const int nb = front_nb_for(qmax, nblocks);
     return nb > 1 ? (qmax + nb - 2) / (nb - 1) + 1 : 0;
 }
 
@@ -927,7 +931,7 @@ void launch_fsp_t(const DevPlan& P, const int32_t* fronts, int nfronts, int batc
 
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st) {
     if (nfronts <= 0) return;
-    const int nb = front_nb_for(qmax);
+    const int nb = front_nb_for(qmax, (int64_t)nfronts * batch);
     const int RS = fs_rows_pad(qmax);
     const size_t smem = fs_smem_bytes(nb, RS);
     // threads per front: one warp for tiny FS blocks (no CTA-wide barriers), 4 or 8 warps above
