@@ -71,6 +71,9 @@ struct kep_ctx {
     int32_t* d_fstate = nullptr;
     int32_t* d_pending = nullptr;                // fronts flagged for a fast-path rerun (per level)
     int4* d_uitems = nullptr;                   // k_fsu tiles (front, I, J, 0)
+    int64_t* d_goff = nullptr;                  // k_fsp global scratch offsets (-1: shared memory)
+    int64_t gscratch_stride = 0;
+    double* d_gscratch = nullptr;
     std::vector<int64_t> uitem_off, uitem_cnt;
     std::vector<int> level_qmax;                // per level: max p + slack over its fast fronts
     std::vector<double> item_flops;             // per level: algorithmic a4 flops of its fast fronts
@@ -146,6 +149,7 @@ void free_batch(kep_ctx* c) {
     cudaFree(c->d_flag); c->d_flag = nullptr;
     cudaFree(c->d_forced); c->d_forced = nullptr;
     cudaFree(c->d_fstate); c->d_fstate = nullptr;
+    cudaFree(c->d_gscratch); c->d_gscratch = nullptr;
     cudaFree(c->d_pending); c->d_pending = nullptr;
 }
 
@@ -154,7 +158,7 @@ kep_status alloc_batch(kep_ctx* c) {
     free_batch(c);
     size_t freeb = 0, totalb = 0;
     KEP_CUDA(c, cudaMemGetInfo(&freeb, &totalb));
-    const size_t per_shift = ((size_t)c->sym.arena_doubles + (size_t)c->aux_stride) * sizeof(double);
+    const size_t per_shift = ((size_t)c->sym.arena_doubles + (size_t)c->aux_stride + (size_t)c->gscratch_stride) * sizeof(double);
     int cap = std::max(1, c->opts.max_batch);
     const size_t budget = (size_t)(0.85 * (double)freeb);
     while (cap > 1 && per_shift * (size_t)cap > budget) cap--;
@@ -174,6 +178,7 @@ kep_status alloc_batch(kep_ctx* c) {
     KEP_CUDA(c, cudaMemset(c->d_flag, 0, nfb));
     KEP_CUDA(c, cudaMalloc(&c->d_forced, nfb * (kep::FMAX + 1)));
     KEP_CUDA(c, cudaMalloc(&c->d_fstate, nfb * kep::FSTATE_W));
+    KEP_CUDA(c, cudaMalloc(&c->d_gscratch, sizeof(double) * std::max<int64_t>(c->gscratch_stride, 1) * cap));
     KEP_CUDA(c, cudaMalloc(&c->d_pending, sizeof(int32_t)));
     c->h_stats.resize(cap);
     return KEP_OK;
@@ -247,6 +252,20 @@ kep_status build_lists(kep_ctx* c) {
     }
     c->aux_stride = std::max<int64_t>(acc, 1) * kep::AUX_W;
     KEP_CUDA(c, upload(&c->d_aux_off, aoff));
+    // global scratch for the k_fsp block columns of levels whose FS blocks exceed shared memory
+    std::vector<int64_t> goff(S.nf > 0 ? S.nf : 1, -1);
+    int64_t gacc = 0;
+    for (int L = 0; L < nl; ++L) {
+        if (!c->fast_cnt[L] || !kep::fs_uses_gls(c->level_qmax[L])) continue;
+        const int64_t per = (int64_t)kep::fs_gls_doubles(16, kep::fs_rows_pad(c->level_qmax[L]));
+        for (int64_t x = c->fast_off[L]; x < c->fast_off[L] + c->fast_cnt[L]; ++x) {
+            goff[fast[x]] = gacc;
+            gacc += per;
+        }
+    }
+    c->gscratch_stride = gacc;
+    cudaFree(c->d_goff); c->d_goff = nullptr;
+    KEP_CUDA(c, upload(&c->d_goff, goff));
     KEP_CUDA(c, upload(&c->d_lists, lists));
     KEP_CUDA(c, upload(&c->d_items, items));
     return KEP_OK;
@@ -367,6 +386,9 @@ DevPlan make_plan(kep_ctx* c) {
     P.forced = c->d_forced;
     P.fstate = c->d_fstate;
     P.pending = c->d_pending;
+    P.gscratch = c->d_gscratch;
+    P.gscratch_stride = c->gscratch_stride;
+    P.goff = c->d_goff;
     P.debug = getenv("KEP_DEBUG") ? 1 : 0;
     return P;
 }
@@ -1274,7 +1296,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
                         c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci,
-                        c->d_csr_a, c->d_csr_b};
+                        c->d_csr_a, c->d_csr_b, c->d_goff};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -54,6 +54,9 @@ struct DevPlan {
     int32_t* forced;             // [batch][nf][FMAX+1] count, then S1 steps at which to delay
     int32_t* fstate;             // [batch][nf][FSTATE_W] k_fsp state: e, qe, step, forced cursor, block start
     int32_t* pending;            // count of fronts flagged FL_RERUN in the current level
+    double* gscratch;            // [batch][gscratch_stride] k_fsp block columns of FS blocks too large for smem
+    int64_t gscratch_stride;
+    const int64_t* goff;         // [nf] scratch offset, -1 = shared memory
     int32_t debug;               // KEP_DEBUG set: diagnostic printf in rare paths
 };
 
@@ -136,6 +139,9 @@ void launch_assemble(const DevPlan& P, const int32_t* fronts, int nfronts, int b
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st);
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 int fs_iters(int qmax, int64_t nblocks);   // k_fsp launches that finish every front of a level
+bool fs_uses_gls(int qmax);                 // the level's block columns live in global scratch
+int fs_rows_pad(int qmax);
+size_t fs_gls_doubles(int nb, int RS);
 void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, cudaStream_t st);
 void launch_fwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
 void launch_bwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);

@@ -161,17 +161,20 @@ struct Smem {
     int* oo;               // [NB] 2x2 partner offset (0 / +1 / -1)
     int* tp;               // [NB] kind per block column
     int* st;               // [NB] S1 step index per block column
-    int* perm;             // [RS] original FS column at each position
     Red* red;
 };
 
+// gls != NULL: the block columns and the two column buffers live in a global
+// scratch area of the front (FS blocks too large for shared memory).
 template <int NB>
-__device__ Smem<NB> carve(double* base, int RS) {
+__device__ Smem<NB> carve(double* base, int RS, double* gls) {
     Smem<NB> S;
     double* p = base;
-    S.Ls = p; p += (size_t)NB * RS;
-    S.wk = p; p += RS;
-    S.wr = p; p += RS;
+    double* g = gls ? gls : base;
+    S.Ls = g; g += (size_t)NB * RS;
+    S.wk = g; g += RS;
+    S.wr = g; g += RS;
+    if (!gls) p = g;
     S.cs = p; p += NB;
     S.co = p; p += NB;
     S.wrow = p; p += NB;
@@ -184,16 +187,17 @@ __device__ Smem<NB> carve(double* base, int RS) {
     S.oo = (int*)p; p += (NB + 1) / 2;
     S.tp = (int*)p; p += (NB + 1) / 2;
     S.st = (int*)p; p += (NB + 1) / 2;
-    S.perm = (int*)p; p += (RS + 1) / 2;
     return S;
 }
 
 }  // namespace
 
-size_t fs_smem_bytes(int nb, int RS) {
-    size_t d = (size_t)nb * RS + 2 * (size_t)RS + 8 * nb + (2 * sizeof(Red) + 7) / 8 + 3 * ((nb + 1) / 2) + (RS + 1) / 2;
+size_t fs_smem_bytes(int nb, int RS, bool gls) {
+    size_t d = (gls ? 0 : (size_t)nb * RS + 2 * (size_t)RS) + 8 * nb + (2 * sizeof(Red) + 7) / 8 + 3 * ((nb + 1) / 2);
     return d * sizeof(double);
 }
+
+size_t fs_gls_doubles(int nb, int RS) { return (size_t)(nb + 2) * RS; }
 
 namespace {
 
@@ -252,9 +256,10 @@ __device__ void do_swap(const Smem<NB>& S, int RS, double* F, int ld, int q, int
 template <int NB, int TH>
 __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict__ fronts, int RS, int mode) {
     extern __shared__ __align__(16) double dyn[];
-    const Smem<NB> S = carve<NB>(dyn, RS);
     const int s = fronts[blockIdx.x];
     const int sh = blockIdx.y;
+    double* gls = P.goff[s] >= 0 ? P.gscratch + (size_t)sh * P.gscratch_stride + P.goff[s] : nullptr;
+    const Smem<NB> S = carve<NB>(dyn, RS, gls);
     const int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
     int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
     const int nd = nd_in[s];
@@ -901,15 +906,18 @@ int fs_rows_pad(int qmax) { return ((qmax + 15) / 16) * 16 + 4; }
 
 // NB for a level whose fronts have at most qmax fully-summed columns (with
 // slack): the widest block whose shared memory fits; 0 = too large.
+bool fs_uses_gls(int qmax) { return fs_smem_bytes(8, fs_rows_pad(qmax), false) > kFsSmemLimit; }
+
 int front_nb_for(int qmax, int64_t nblocks) {
     const int RS = fs_rows_pad(qmax);
     const size_t lim = kFsSmemLimit;
+    if (fs_uses_gls(qmax)) return 16;                  // block columns in global scratch
     // NB = 32 halves the k_fsu passes but its Ls block (q x 32) leaves one CTA per SM for q > 384:
     // worth it only when the level is too small to fill the GPU anyway
     const int q32 = nblocks < 4 * 148 ? 640 : 384;
-    if (fs_smem_bytes(32, RS) <= lim && qmax <= q32) return 32;
-    if (fs_smem_bytes(16, RS) <= lim) return 16;
-    if (fs_smem_bytes(8, RS) <= lim) return 8;
+    if (fs_smem_bytes(32, RS, false) <= lim && qmax <= q32) return 32;
+    if (fs_smem_bytes(16, RS, false) <= lim) return 16;
+    if (fs_smem_bytes(8, RS, false) <= lim) return 8;
     return 0;
 }
 
@@ -933,7 +941,7 @@ void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch,
     if (nfronts <= 0) return;
     const int nb = front_nb_for(qmax, (int64_t)nfronts * batch);
     const int RS = fs_rows_pad(qmax);
-    const size_t smem = fs_smem_bytes(nb, RS);
+    const size_t smem = fs_smem_bytes(nb, RS, fs_uses_gls(qmax));
     // threads per front: one warp for tiny FS blocks (no CTA-wide barriers), 4 or 8 warps above
     const int th = qmax <= 40 ? 32 : (qmax <= 192 ? 128 : 256);
 #define KEP_FSP(NBV, THV) if (nb == NBV && th == THV) return launch_fsp_t<NBV, THV>(P, fronts, nfronts, batch, RS, smem, mode, st)

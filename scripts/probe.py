@@ -27,3 +27,5 @@ for w in which:
     if w == "c1": run(kepgen.config(1), 32)
     if w == "c2": run(kepgen.config(2), 16)
     if w == "c4s": run(kepgen.tb_pencil(shape=(10, 10, 400), o=4, periodic=(False, False, True), seed=4), 16)
+    if w == "c3": run(kepgen.config(3), 8, batch=8)
+    if w == "c5": run(kepgen.config(5), 4, batch=4)
