@@ -179,7 +179,7 @@ kep_status alloc_batch(kep_ctx* c) {
     KEP_CUDA(c, cudaMalloc(&c->d_forced, nfb * (kep::FMAX + 1)));
     KEP_CUDA(c, cudaMalloc(&c->d_fstate, nfb * kep::FSTATE_W));
     KEP_CUDA(c, cudaMalloc(&c->d_gscratch, sizeof(double) * std::max<int64_t>(c->gscratch_stride, 1) * cap));
-    KEP_CUDA(c, cudaMalloc(&c->d_pending, sizeof(int32_t)));
+    KEP_CUDA(c, cudaMalloc(&c->d_pending, 2 * sizeof(int32_t)));
     c->h_stats.resize(cap);
     return KEP_OK;
 }
@@ -477,15 +477,19 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 const int nfl2 = (int)c->fast_cnt[L];
                 // pass 0, then kReruns passes over the fronts whose full-column test failed
                 // (each with one more forced delay), then the unblocked kernel for the rest
-                const int iters = kep::fs_iters(c->level_qmax[L], (int64_t)nfl2 * m);
+                int iters = kep::fs_iters(c->level_qmax[L], (int64_t)nfl2 * m);
                 for (int pass = 0; pass <= kReruns; ++pass) {
                     if (pass > 0) {                     // any front flagged for a rerun at this level?
-                        int32_t pend = 0;
-                        KEP_CUDA(c, cudaMemcpyAsync(&pend, c->d_pending, sizeof(pend), cudaMemcpyDeviceToHost, c->stream));
+                        int32_t pend[2] = {0, 0};
+                        KEP_CUDA(c, cudaMemcpyAsync(pend, c->d_pending, sizeof(pend), cudaMemcpyDeviceToHost, c->stream));
                         KEP_CUDA(c, cudaStreamSynchronize(c->stream));
-                        if (pend == 0) break;
+                        if (pend[0] == 0) break;
+                        // the rerun pass only needs the pivot blocks of the largest flagged FS block
+                        // (at the level's block width)
+                        const int nbl = kep::front_nb_for(c->level_qmax[L], (int64_t)nfl2 * m);
+                        iters = std::min(iters, (pend[1] + nbl - 2) / (nbl - 1) + 1);
                     }
-                    KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, sizeof(int32_t), c->stream));
+                    KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
                     for (int itn = 0; itn < iters; ++itn) {
                         mark(KEP_K_PANEL, true);
                         kep::launch_fsp(P, fl, nfl2, m, c->level_qmax[L], itn == 0 ? (pass == 0 ? 0 : 1) : 2, c->stream);

@@ -253,13 +253,13 @@ __device__ void do_swap(const Smem<NB>& S, int RS, double* F, int ld, int q, int
 // mode 1: first block of a rerun pass; mode 2: next block).  The state between
 // launches (e, qe, S1 step, forced-delay cursor, block start) lives in fstate.
 // TH threads per front (one warp for tiny FS blocks).
-template <int NB, int TH>
+template <int NB, int TH, bool GLS>
 __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict__ fronts, int RS, int mode) {
     extern __shared__ __align__(16) double dyn[];
     const int s = fronts[blockIdx.x];
     const int sh = blockIdx.y;
-    double* gls = P.goff[s] >= 0 ? P.gscratch + (size_t)sh * P.gscratch_stride + P.goff[s] : nullptr;
-    const Smem<NB> S = carve<NB>(dyn, RS, gls);
+    // compile-time choice: with GLS = false every block-column access is a shared-memory access
+    const Smem<NB> S = carve<NB>(dyn, RS, GLS ? P.gscratch + (size_t)sh * P.gscratch_stride + P.goff[s] : nullptr);
     const int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
     int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
     const int nd = nd_in[s];
@@ -888,6 +888,7 @@ __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restri
                 forced[0] = nf_ + 1;
                 *flag = FL_RERUN;
                 atomicAdd(P.pending, 1);
+                atomicMax(P.pending + 1, q);                 // largest FS block to rerun (iteration count)
             } else {
                 *flag = FL_REF;
             }
@@ -926,25 +927,27 @@ int fs_iters(int qmax, int64_t nblocks) {
     return nb > 1 ? (qmax + nb - 2) / (nb - 1) + 1 : 0;
 }
 
-template <int NB, int TH>
+template <int NB, int TH, bool GLS>
 void launch_fsp_t(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int RS, size_t smem, int mode,
                   cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_fsp<NB, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
+        cudaFuncSetAttribute(k_fsp<NB, TH, GLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
         attr = true;
     }
-    k_fsp<NB, TH><<<dim3(nfronts, batch), TH, smem, st>>>(P, fronts, RS, mode);
+    k_fsp<NB, TH, GLS><<<dim3(nfronts, batch), TH, smem, st>>>(P, fronts, RS, mode);
 }
 
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st) {
     if (nfronts <= 0) return;
     const int nb = front_nb_for(qmax, (int64_t)nfronts * batch);
     const int RS = fs_rows_pad(qmax);
-    const size_t smem = fs_smem_bytes(nb, RS, fs_uses_gls(qmax));
+    const bool gls = fs_uses_gls(qmax);
+    const size_t smem = fs_smem_bytes(nb, RS, gls);
+    if (gls) return launch_fsp_t<16, 256, true>(P, fronts, nfronts, batch, RS, smem, mode, st);
     // threads per front: one warp for tiny FS blocks (no CTA-wide barriers), 4 or 8 warps above
     const int th = qmax <= 40 ? 32 : (qmax <= 192 ? 128 : 256);
-#define KEP_FSP(NBV, THV) if (nb == NBV && th == THV) return launch_fsp_t<NBV, THV>(P, fronts, nfronts, batch, RS, smem, mode, st)
+#define KEP_FSP(NBV, THV) if (nb == NBV && th == THV) return launch_fsp_t<NBV, THV, false>(P, fronts, nfronts, batch, RS, smem, mode, st)
     KEP_FSP(32, 32); KEP_FSP(32, 128); KEP_FSP(32, 256);
     KEP_FSP(16, 32); KEP_FSP(16, 128); KEP_FSP(16, 256);
     KEP_FSP(8, 32); KEP_FSP(8, 128); KEP_FSP(8, 256);
