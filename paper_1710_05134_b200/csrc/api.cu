@@ -74,7 +74,8 @@ struct kep_ctx {
     int64_t* d_goff = nullptr;                  // k_fsp global scratch offsets (-1: shared memory)
     int64_t gscratch_stride = 0;
     double* d_gscratch = nullptr;
-    std::vector<int64_t> uitem_off, uitem_cnt;
+    std::vector<int64_t> uitem_off, uitem_cnt, small_off, small_cnt;
+    int32_t* d_small = nullptr;                  // fronts whose Schur update runs in k_schur_small
     std::vector<int> level_qmax;                // per level: max p + slack over its fast fronts
     std::vector<double> item_flops;             // per level: algorithmic a4 flops of its fast fronts
     std::vector<kep_factorization*> factors;    // live factors (released by kep_destroy)
@@ -192,8 +193,10 @@ kep_status build_lists(kep_ctx* c) {
     const bool use_fast = c->opts.kernel_variant == 0;
     std::vector<int32_t> fast, ref;
     std::vector<int4> items, litems, uitems;
+    std::vector<int32_t> small;
     c->litem_off.assign(nl, 0); c->litem_cnt.assign(nl, 0);
     c->uitem_off.assign(nl, 0); c->uitem_cnt.assign(nl, 0);
+    c->small_off.assign(nl, 0); c->small_cnt.assign(nl, 0);
     c->fast_off.assign(nl, 0); c->fast_cnt.assign(nl, 0);
     c->ref_off.assign(nl, 0); c->ref_cnt.assign(nl, 0);
     c->item_off.assign(nl, 0); c->item_cnt.assign(nl, 0);
@@ -204,6 +207,7 @@ kep_status build_lists(kep_ctx* c) {
         c->item_off[L] = (int64_t)items.size();
         c->litem_off[L] = (int64_t)litems.size();
         c->uitem_off[L] = (int64_t)uitems.size();
+        c->small_off[L] = (int64_t)small.size();
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
             const int s = S.level_fronts[k];
             const int qcap = S.capacity[s] - S.ncb[s];            // p + slack
@@ -213,9 +217,13 @@ kep_status build_lists(kep_ctx* c) {
                 for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) litems.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
                 for (int I = 0; I < (qcap + 63) / 64; ++I)
                     for (int J = 0; J <= I; ++J) uitems.push_back(make_int4(s, I, J, 0));
-                const int nt = (S.ncb[s] + 63) / 64;
-                for (int I = 0; I < nt; ++I)
-                    for (int J = 0; J <= I; ++J) items.push_back(make_int4(s, I, J, 0));
+                if (kep::schur_small_ok(S.ncb[s], qcap)) {
+                    small.push_back(s);                                  // whole CB in one CTA
+                } else {
+                    const int nt = (S.ncb[s] + 63) / 64;
+                    for (int I = 0; I < nt; ++I)
+                        for (int J = 0; J <= I; ++J) items.push_back(make_int4(s, I, J, 0));
+                }
             } else {
                 ref.push_back(s);
             }
@@ -225,6 +233,7 @@ kep_status build_lists(kep_ctx* c) {
         c->item_cnt[L] = (int64_t)items.size() - c->item_off[L];
         c->litem_cnt[L] = (int64_t)litems.size() - c->litem_off[L];
         c->uitem_cnt[L] = (int64_t)uitems.size() - c->uitem_off[L];
+        c->small_cnt[L] = (int64_t)small.size() - c->small_off[L];
     }
     c->item_flops.assign(nl, 0.0);
     for (int L = 0; L < nl; ++L)
@@ -241,6 +250,8 @@ kep_status build_lists(kep_ctx* c) {
     cudaFree(c->d_litems); c->d_litems = nullptr;
     cudaFree(c->d_uitems); c->d_uitems = nullptr;
     KEP_CUDA(c, upload(&c->d_uitems, uitems));
+    cudaFree(c->d_small); c->d_small = nullptr;
+    KEP_CUDA(c, upload(&c->d_small, small));
     cudaFree(c->d_aux_off); c->d_aux_off = nullptr;
     KEP_CUDA(c, upload(&c->d_litems, litems));
     // pivot-record offsets: Q_s = p_s + slack entries per front
@@ -530,11 +541,12 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 c->prof.launches[KEP_K_REF]++;
             }
             if (keep) kep::launch_store(P, keep->plan(), c->d_level_fronts + b, nfl, c->stream);
-            if (c->item_cnt[L]) {
+            if (c->item_cnt[L] || c->small_cnt[L]) {
                 mark(KEP_K_SCHUR, true);
                 kep::launch_schur(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
+                kep::launch_schur_small(P, c->d_small + c->small_off[L], (int)c->small_cnt[L], m, c->stream);
                 mark(KEP_K_SCHUR, false);
-                c->prof.launches[KEP_K_SCHUR]++;
+                c->prof.launches[KEP_K_SCHUR] += (c->item_cnt[L] ? 1 : 0) + (c->small_cnt[L] ? 1 : 0);
                 c->prof.schur_flops += c->item_flops[L] * m;
             }
         }
@@ -1300,7 +1312,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
                         c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci,
-                        c->d_csr_a, c->d_csr_b, c->d_goff};
+                        c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

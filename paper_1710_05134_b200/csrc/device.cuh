@@ -159,6 +159,8 @@ void launch_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 int front_nb_for(int qmax, int64_t nblocks = 0);   // block width (0: too large, use the reference kernel)
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
+void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
+bool schur_small_ok(int c, int qcap);     // front handled by k_schur_small
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,
                         bool only_flagged = false);
 void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st);

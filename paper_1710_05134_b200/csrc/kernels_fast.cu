@@ -119,6 +119,86 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
             }
 }
 
+// Small fronts (c <= 256, FS block <= 48): one CTA per front, the CB's G rows
+// staged in shared memory once, every 32 x 32 lower tile of the CB computed from
+// them (DMMA), RED epilogue.  Avoids the per-tile setup and the repeated operand
+// loads of k_schur where K (= pivots) is a single chunk.
+constexpr int SS_T = 256;
+constexpr int SS_C = 256;       // max CB order
+constexpr int SS_K = 48;        // max eliminated pivots
+constexpr int SS_P = SS_K + 4;  // = 4 (mod 16)
+
+__global__ void __launch_bounds__(SS_T) k_schur_small(DevPlan P, const int32_t* __restrict__ fronts) {
+    extern __shared__ __align__(16) double Gs[];        // [SS_C][SS_P]
+    __shared__ unsigned long long Sg[SS_K];
+    const int s = fronts[blockIdx.x];
+    const int sh = blockIdx.y;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    if (nd < 0) return;
+    if (P.flag[(size_t)sh * P.nf + s] != FL_OK) return;
+    const int ndo = P.nd_out[(size_t)sh * P.nf + s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const int e = q - ndo;
+    if (e <= 0 || c <= 0) return;
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, tg = lane & 3;
+    const int K4 = (e + 3) & ~3;
+    for (int x = tid; x < c * K4; x += SS_T) {            // G rows of the CB (upper part), zero-padded to K4
+        const int i = x / K4, t = x - i * K4;
+        const bool v = t < e;
+        cp_async8(&Gs[i * SS_P + t], F + (v ? (t + (size_t)(q + i) * ld) : 0), v);
+    }
+    cp_async_commit();
+    if (tid < SS_K) Sg[tid] = (tid < e && A.sgn[tid] < 0.0) ? 0x8000000000000000ull : 0ull;
+    cp_async_wait<0>();
+    __syncthreads();
+    const int T = (c + 31) >> 5;
+    const int ntile = T * (T + 1) / 2;
+    for (int tile = warp; tile < ntile; tile += SS_T / 32) {
+        int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+        while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+        while (I * (I + 1) / 2 > tile) --I;
+        const int J = tile - I * (I + 1) / 2;
+        const int i0 = 32 * I, j0 = 32 * J;
+        double acc[4][4][2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int k4 = 0; k4 < K4; k4 += 4) {
+            double a[4], b[4];
+            const long long sm = (long long)Sg[k4 + tg];
+#pragma unroll
+            for (int mb = 0; mb < 4; ++mb) {
+                const int i = i0 + 8 * mb + g;
+                a[mb] = i < c ? Gs[i * SS_P + k4 + tg] : 0.0;
+            }
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) {
+                const int j = j0 + 8 * nb + g;
+                b[nb] = j < c ? __longlong_as_double(__double_as_longlong(Gs[j * SS_P + k4 + tg]) ^ sm) : 0.0;
+            }
+#pragma unroll
+            for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb], a[mb], b[nb]);
+        }
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int i = i0 + 8 * mb + g;
+                    const int j = j0 + 8 * nb + 2 * tg + h;
+                    if (i < c && j < c && i >= j) atomicAdd(&F[(q + i) + (size_t)(q + j) * ld], -acc[mb][nb][h]);
+                }
+    }
+}
+
 }  // namespace
 
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
@@ -126,4 +206,16 @@ void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cu
     k_schur<<<dim3(nitems, batch), SCH_T, 0, st>>>(P, items);
 }
 
+}  // namespace kep
+
+namespace kep {
+bool schur_small_ok(int c, int qcap) { return c > 0 && c <= SS_C && qcap <= SS_K; }
+
+void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    const size_t smem = sizeof(double) * SS_C * SS_P;
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(k_schur_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+    k_schur_small<<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts);
+}
 }  // namespace kep
