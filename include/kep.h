@@ -238,6 +238,10 @@ typedef struct {
     uint64_t seed;              /* seed of the start vectors (splitmix64, uniform(-1,1)) when v0s are NULL */
     const double* v0_stage1;    /* optional start vector of stage 1 (n, host) */
     const double* v0_stage3;    /* optional start vector of stage 3 (n, host) */
+    int32_t bisect_only;        /* 1: "straightforward bisection":
+                                   stage 2 stops when (sigma_u - sigma_l) / max(|sigma_l|, |sigma_u|) <
+                                   bisect_rtol, lambda = the midpoint, no stage 3, x not written */
+    double bisect_rtol;         /* default 1e-14 */
 } kep_kth_opts;
 
 typedef struct {

@@ -943,6 +943,8 @@ void kep_default_kth_opts(kep_kth_opts* o) {
     o->max_si = 500;
     o->shifts_per_round = 1;
     o->seed = 1;
+    o->bisect_only = 0;
+    o->bisect_rtol = 1e-14;
 }
 
 namespace {
@@ -1090,9 +1092,16 @@ kep_status kep_kth_eigenpair(kep_ctx* c, int64_t k, const kep_kth_opts* opts_in,
     std::vector<double> sg(P);
     std::vector<int64_t> nv(P);
     std::vector<kep_status> ps(P);
-    while (nhi - nlo > o.m_max) {
-        if (R.stage2_rounds >= o.max_bisect || hi - lo <= 4.0 * DBL_EPSILON * std::max(std::fabs(lo), std::fabs(hi))) {
-            R.status = KEP_ECLUSTER;
+    auto narrow_more = [&]() -> bool {
+        if (o.bisect_only)                                                   // PAPER.md:674-676 footnote
+            return (hi - lo) / std::max(std::fabs(lo), std::fabs(hi)) >= o.bisect_rtol;
+        return nhi - nlo > o.m_max;                                          // Alg. 1' line 1
+    };
+    const int max_rounds = o.bisect_only ? std::max(o.max_bisect, 256) : o.max_bisect;
+    while (narrow_more()) {
+        if (R.stage2_rounds >= max_rounds ||
+            (!o.bisect_only && hi - lo <= 4.0 * DBL_EPSILON * std::max(std::fabs(lo), std::fabs(hi)))) {
+            R.status = o.bisect_only ? KEP_ENOCONV : KEP_ECLUSTER;
             break;
         }
         for (int i = 0; i < P; ++i) sg[i] = lo + (hi - lo) * (double)(i + 1) / (double)(P + 1);
@@ -1118,6 +1127,12 @@ kep_status kep_kth_eigenpair(kep_ctx* c, int64_t k, const kep_kth_opts* opts_in,
     R.sigma_lower = lo; R.sigma_upper = hi; R.nu_lower = nlo; R.nu_upper = nhi;
     R.seconds[1] = now_s() - t0;
     if (R.status != KEP_OK) {
+        if (rep_out) *rep_out = R;
+        return KEP_OK;
+    }
+    if (o.bisect_only) {                                                     // lambda_k = midpoint, no stage 3
+        *lambda = 0.5 * (lo + hi);
+        R.eta = 0.5 * (hi - lo);
         if (rep_out) *rep_out = R;
         return KEP_OK;
     }

@@ -66,7 +66,8 @@ class _KthOpts(C.Structure):
     _fields_ = [("m_max", C.c_int32), ("tau_res", C.c_double), ("tau_diff", C.c_double),
                 ("max_lanczos", C.c_int32), ("max_bisect", C.c_int32), ("max_si", C.c_int32),
                 ("shifts_per_round", C.c_int32), ("seed", C.c_uint64),
-                ("v0_stage1", C.POINTER(C.c_double)), ("v0_stage3", C.POINTER(C.c_double))]
+                ("v0_stage1", C.POINTER(C.c_double)), ("v0_stage3", C.POINTER(C.c_double)),
+                ("bisect_only", C.c_int32), ("bisect_rtol", C.c_double)]
 
 
 class _KthReport(C.Structure):
@@ -270,13 +271,15 @@ class Kep:
         return Factor(self, h)
 
     def kth_eigenpair(self, k: int, m_max=20, tau_res=1e-10, tau_diff=1e-10, max_lanczos=64, max_bisect=128,
-                      max_si=500, shifts_per_round=1, seed=1, v0_stage1=None, v0_stage3=None, want_x=True):
+                      max_si=500, shifts_per_round=1, seed=1, v0_stage1=None, v0_stage3=None, want_x=True,
+                      bisect_only=False, bisect_rtol=1e-14):
         """kep_kth_eigenpair: (lambda_k or None, x or None, report dict)."""
         o = _KthOpts()
         lib().kep_default_kth_opts(C.byref(o))
         o.m_max, o.tau_res, o.tau_diff = int(m_max), float(tau_res), float(tau_diff)
         o.max_lanczos, o.max_bisect, o.max_si = int(max_lanczos), int(max_bisect), int(max_si)
         o.shifts_per_round, o.seed = int(shifts_per_round), int(seed)
+        o.bisect_only, o.bisect_rtol = int(bool(bisect_only)), float(bisect_rtol)
         keep = []
         for name, v in (("v0_stage1", v0_stage1), ("v0_stage3", v0_stage3)):
             if v is not None:
@@ -294,7 +297,7 @@ class Kep:
         rep = {f: getattr(rp, f) for f, _ in _KthReport._fields_ if f != "seconds"}
         rep["seconds"] = list(rp.seconds)
         ok = rp.status == KEP_OK
-        return (lam.value if ok else None), (x if ok else None), rep
+        return (lam.value if ok else None), (x if ok and not bisect_only else None), rep
 
     def perm(self) -> np.ndarray:
         p = np.empty(self.n, dtype=np.int64)

@@ -28,4 +28,4 @@ for w in which:
     if w == "c2": run(kepgen.config(2), 16)
     if w == "c4s": run(kepgen.tb_pencil(shape=(10, 10, 400), o=4, periodic=(False, False, True), seed=4), 16)
     if w == "c3": run(kepgen.config(3), 8, batch=8)
-    if w == "c5": run(kepgen.config(5), 4, batch=4)
+    if w == "c5": run(kepgen.config(5), 2, batch=2)

@@ -94,3 +94,34 @@ def test_c2_kth_validated():
     Bf = Lo_b + sp.tril(Lo_b, -1).T
     assert np.linalg.norm(Af @ x - lam * (Bf @ x)) / np.linalg.norm(x) < 1e-9
     assert rep["eta"] <= 1e-10 * abs(lam) + 1e-14
+
+
+@pytest.mark.parametrize("kk,P", [(300, 1), (700, 3)])
+def test_c1_straightforward_bisection(kk, P):
+    """f4: bisection alone to a relative interval length < 1e-14 (PAPER.md:674-676);
+    the paper reports 47-49 iterations for that criterion on its matrices."""
+    p = kepgen.config(1)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    lam, x, rep = k.kth_eigenpair(kk, shifts_per_round=P, bisect_only=True, v0_stage1=_start(p.n, 11))
+    assert rep["status"] == KEP_OK and x is None
+    assert abs(lam - w[kk - 1]) <= 1e-12 * abs(w[kk - 1])
+    assert (rep["sigma_upper"] - rep["sigma_lower"]) / max(abs(rep["sigma_lower"]), abs(rep["sigma_upper"])) < 1e-14
+    assert rep["nu_lower"] < kk <= rep["nu_upper"]
+    # oracle Alg. 1 (interval-length criterion) from the same stage-1 interval: the same number of
+    # midpoints up to the last few, whose counts sit within rounding of lambda_k
+    nu = lambda s: oracle.nu_eig(A, B, s, eigvals=w)
+    lo, hi = rep["s1_lower"], rep["s1_upper"]
+    if P == 1:
+        it = 0
+        while (hi - lo) / max(abs(lo), abs(hi)) >= 1e-14:
+            s = 0.5 * (lo + hi)
+            if kk <= nu(s):
+                hi = s
+            else:
+                lo = s
+            it += 1
+        assert abs(it - rep["stage2_rounds"]) <= 2
+        assert abs(0.5 * (lo + hi) - lam) <= 1e-13 * abs(lam)
