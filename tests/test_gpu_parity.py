@@ -184,3 +184,20 @@ def test_twin_c4_geometry_full_size():
     nus, st = k.inertia_many(sig)
     assert np.all(st == KEP_OK)
     assert np.array_equal(nus, oracle.nu_twin(q.meta["twin"], sig, w))
+
+
+def test_twin_c5_geometry_full_size():
+    """n = 500k closed-form twin with the c5 geometry (50^3, o = 4) and the cutoff-2.2-like
+    27+6-point pattern: root FS block ~20k columns, i.e. the global-scratch pivot-block path
+    of k_fsp (FS blocks too large for shared memory) and the multi-CTA trailing updates."""
+    q = kepgen.twin_pencil((50, 50, 50), 4, uA=0.08, uB=0.01, seed=105)
+    w = oracle.twin_eigenvalues(q.meta["twin"])
+    sig = kepgen.uniform_shifts(w[0], w[-1], 6)
+    sig = sig[_certified(w, sig)][:4]
+    assert sig.shape[0] >= 2
+    k = Kep.from_pencil(q, max_batch=2)
+    assert k.analysis()["max_front"] > 4000
+    k.set_values(q.a, q.b)
+    nus, st = k.inertia_many(sig)
+    assert np.all(st == KEP_OK)
+    assert np.array_equal(nus, oracle.nu_twin(q.meta["twin"], sig, w))
