@@ -814,67 +814,79 @@ __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restri
     ShiftStat* st = P.stats + sh;
     const double u = P.u;
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        unsigned long long c_neg = 0, c_zero = 0, c_pos = 0, c_2x2 = 0;
-        double minpiv = DBL_MAX;
+    // every pivot's test in parallel (the tests are independent given the stored maxima);
+    // the first failure in pivot order is a block-wide min, the inertia a block-wide sum
+    __shared__ int s_first;
+    __shared__ unsigned long long s_cnt[4];
+    __shared__ unsigned long long s_minb;
+    if (tid == 0) { s_first = INT_MAX; s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0ull; s_minb = ~0ull; }
+    __syncthreads();
+    unsigned long long c_neg = 0, c_zero = 0, c_pos = 0, c_2x2 = 0;
+    double minpiv = DBL_MAX;
+    int first = INT_MAX;
+    for (int t = tid; t < e; t += FT) {
+        const int kd = A.kind[t];
+        if (kd == PK_2X2B) continue;                      // tested with its first column
+        const double ca = root ? 0.0 : __longlong_as_double((long long)A.cm[t]);
         bool ok = true;
-        int tfail = -1;
-        for (int t = 0; t < e && ok;) {
-            const int kd = A.kind[t];
-            const double ca = root ? 0.0 : __longlong_as_double((long long)A.cm[t]);
-            const int t0 = t;
-            if (kd == PK_ZERO) {
-                ok = ca == 0.0;
-                c_zero++;
-                minpiv = 0.0;
-                t += 1;
-            } else if (kd == PK_1X1) {
-                const double d = A.d[t];
-                ok = root || fabs(d) >= u * fmax(A.fa[t], ca);
-                if (d < 0.0) c_neg++; else if (d > 0.0) c_pos++; else c_zero++;
-                minpiv = fmin(minpiv, fabs(d));
-                t += 1;
-            } else {
-                const double d11 = A.d[t], d21 = A.ds[t], d22 = A.d[t + 1];
-                const double det = d11 * d22 - d21 * d21;
-                if (!root) {
-                    const double cb = __longlong_as_double((long long)A.cm[t + 1]);
-                    const double gk = fmax(A.fa[t], ca), gr = fmax(A.fb[t], cb);
-                    if (det == 0.0) ok = false;
-                    else {
-                        const double ad = fabs(det);
-                        ok = (fabs(d22) * gk + fabs(d21) * gr) / ad <= 1.0 / u &&
-                             (fabs(d21) * gk + fabs(d11) * gr) / ad <= 1.0 / u;
-                    }
+        if (kd == PK_ZERO) {
+            ok = ca == 0.0;
+            c_zero++;
+            minpiv = 0.0;
+        } else if (kd == PK_1X1) {
+            const double d = A.d[t];
+            ok = root || fabs(d) >= u * fmax(A.fa[t], ca);
+            if (d < 0.0) c_neg++; else if (d > 0.0) c_pos++; else c_zero++;
+            minpiv = fmin(minpiv, fabs(d));
+        } else {
+            const double d11 = A.d[t], d21 = A.ds[t], d22 = A.d[t + 1];
+            const double det = d11 * d22 - d21 * d21;
+            if (!root) {
+                const double cb = __longlong_as_double((long long)A.cm[t + 1]);
+                const double gk = fmax(A.fa[t], ca), gr = fmax(A.fb[t], cb);
+                if (det == 0.0) ok = false;
+                else {
+                    const double ad = fabs(det);
+                    ok = (fabs(d22) * gk + fabs(d21) * gr) / ad <= 1.0 / u &&
+                         (fabs(d21) * gk + fabs(d11) * gr) / ad <= 1.0 / u;
                 }
-                const double tt = (d11 / d21) * (d22 / d21) - 1.0;
-                if (tt < 0.0) { c_neg++; c_pos++; }
-                else if (tt > 0.0) { if (d11 < 0.0) c_neg += 2; else c_pos += 2; }
-                else { c_zero++; if (d11 + d22 < 0.0) c_neg++; else c_pos++; }
-                const double tr = 0.5 * (d11 + d22);
-                const double disc = sqrt(0.25 * (d11 - d22) * (d11 - d22) + d21 * d21);
-                const double big = fabs(tr) + disc;
-                minpiv = fmin(minpiv, big > 0.0 ? fabs(det) / big : 0.0);
-                c_2x2++;
-                t += 2;
             }
-            if (!ok) tfail = t0;
-            if (!ok && P.debug)
-                printf("[kep] test fails: front %d shift %d pos %d kind %d d=%.3e ds=%.3e fa=%.3e fb=%.3e cm=%.3e cm1=%.3e\n",
-                       s, sh, t0, kd, A.d[t0], A.ds[t0], A.fa[t0], A.fb[t0], ca,
-                       __longlong_as_double((long long)A.cm[t0 + 1 < e ? t0 + 1 : t0]));
+            const double tt = (d11 / d21) * (d22 / d21) - 1.0;
+            if (tt < 0.0) { c_neg++; c_pos++; }
+            else if (tt > 0.0) { if (d11 < 0.0) c_neg += 2; else c_pos += 2; }
+            else { c_zero++; if (d11 + d22 < 0.0) c_neg++; else c_pos++; }
+            const double tr = 0.5 * (d11 + d22);
+            const double disc = sqrt(0.25 * (d11 - d22) * (d11 - d22) + d21 * d21);
+            const double big = fabs(tr) + disc;
+            minpiv = fmin(minpiv, big > 0.0 ? fabs(det) / big : 0.0);
+            c_2x2++;
         }
+        if (!ok) {
+            first = min(first, t);
+            if (P.debug)
+                printf("[kep] test fails: front %d shift %d pos %d kind %d d=%.3e ds=%.3e fa=%.3e fb=%.3e cm=%.3e\n",
+                       s, sh, t, kd, A.d[t], A.ds[t], A.fa[t], A.fb[t], ca);
+        }
+    }
+    if (first < INT_MAX) atomicMin(&s_first, first);
+    if (c_neg) atomicAdd(&s_cnt[0], c_neg);
+    if (c_zero) atomicAdd(&s_cnt[1], c_zero);
+    if (c_pos) atomicAdd(&s_cnt[2], c_pos);
+    if (c_2x2) atomicAdd(&s_cnt[3], c_2x2);
+    if (minpiv < DBL_MAX) atomicMin(&s_minb, (unsigned long long)__double_as_longlong(minpiv));
+    __syncthreads();
+    if (tid == 0) {
+        const bool ok = s_first == INT_MAX;
         s_ok = ok;
-        s_fail = tfail;
-        if (!ok && P.debug)
-            printf("[kep] redo front %d shift %d: q=%d e=%d c=%d\n", s, sh, q, e, c);
+        s_fail = s_first;
+        if (!ok && P.debug) printf("[kep] redo front %d shift %d: q=%d e=%d c=%d\n", s, sh, q, e, c);
         if (ok) {
-            if (c_neg) atomicAdd(&st->n_neg, c_neg);
-            if (c_zero) atomicAdd(&st->n_zero, c_zero);
-            if (c_pos) atomicAdd(&st->n_pos, c_pos);
-            if (c_2x2) atomicAdd(&st->n_2x2, c_2x2);
+            if (s_cnt[0]) atomicAdd(&st->n_neg, s_cnt[0]);
+            if (s_cnt[1]) atomicAdd(&st->n_zero, s_cnt[1]);
+            if (s_cnt[2]) atomicAdd(&st->n_pos, s_cnt[2]);
+            if (s_cnt[3]) atomicAdd(&st->n_2x2, s_cnt[3]);
             if (ndo) atomicAdd(&st->n_delayed, (unsigned long long)ndo);
-            if (minpiv < DBL_MAX) atomic_min_pos_double(&st->minpiv_bits, minpiv);
+            if (s_minb != ~0ull) atomic_min_pos_double(&st->minpiv_bits, __longlong_as_double((long long)s_minb));
         }
     }
     __syncthreads();
