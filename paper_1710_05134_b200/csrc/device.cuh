@@ -111,6 +111,10 @@ __device__ __forceinline__ void pair_eig(double d11, double d21, double d22, dou
     l2 = d11 * sn * sn - 2.0 * d21 * cs * sn + d22 * cs * cs;
 }
 
+// Leading dimension of a front of order f: even, so rows start 16-byte aligned
+// (arena offsets are 256-byte aligned) and the GEMM kernels stage with 16-byte copies.
+__host__ __device__ __forceinline__ int ldpad(int f) { return (f + 1) & ~1; }
+
 __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
     atomicMax(addr, (unsigned long long)__double_as_longlong(v));
 }

@@ -114,8 +114,8 @@ __device__ __forceinline__ void tri_split(int ld, int S, int x, int& lo, int& hi
 // owns the parent columns [lo, hi): zero-fill, original entries (alpha a - sigma b),
 // then the children's CB entries landing in those columns, children in order.
 // Each parent entry belongs to one CTA, so the sum order is fixed (deterministic).
-__global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32_t* __restrict__ list, int S,
-                                                          int only_flagged) {
+__device__ __forceinline__ void assemble_front(const DevPlan& P, const int32_t* __restrict__ list, int S,
+                                               int only_flagged) {
     const int s = list[blockIdx.x / S];
     const int xs = blockIdx.x % S;
     const int sh = blockIdx.y;
@@ -153,11 +153,11 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32
     }
     __syncthreads();
     if (s_skip) return;
-    const int nd = s_nd, p = P.npiv[s], ld = P.forder[s] + nd;
+    const int nd = s_nd, p = P.npiv[s], fo = P.forder[s] + nd, ld = ldpad(fo);   // order, leading dimension
     double* F = arena + P.arena_off[s];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAsmThreads / 32;
     int clo, chi;
-    tri_split(ld, S, xs, clo, chi);
+    tri_split(fo, S, xs, clo, chi);
     if (xs == 0) {   // labels of the FS positions: own pivots, then each child's delayed variables
         const AuxRec A = aux_rec(P, sh, s, P.cap[s] - P.ncb[s]);
         for (int i = threadIdx.x; i < p; i += kAsmThreads) A.label[i] = P.piv_first[s] + i;
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32
         }
     }
     for (int j = clo + warp; j < chi; j += nw)
-        for (int i = j + lane; i < ld; i += 32) F[i + (size_t)j * ld] = 0.0;
+        for (int i = j + lane; i < fo; i += 32) F[i + (size_t)j * ld] = 0.0;
     __syncthreads();
     const double sigma = P.sigma[sh], alpha = P.alpha[sh];
     double mx = 0.0;
@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32
     for (int q = c0; q < c1; ++q) {
         const int c = P.child_list[q];
         const int ndo = nd_out[c];
-        const int fc = P.forder[c] + nd_in[c];
+        const int fc = P.forder[c] + nd_in[c];       // child order
+        const int ldc = ldpad(fc);                   // child leading dimension
         const int mc = ndo + P.ncb[c];
         const int ec = fc - mc;
         const double* __restrict__ Fc = arena + P.arena_off[c];
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32
             // non-delayed child columns land in parent column pj (positions increase with the
             // child index there); delayed columns are filtered entry by entry
             if (j >= ndo && (pj < clo || pj >= chi)) continue;
-            const double* __restrict__ colc = Fc + (size_t)(ec + j) * fc + ec;
+            const double* __restrict__ colc = Fc + (size_t)(ec + j) * ldc + ec;
             for (int i0 = j; i0 < mc; i0 += 32 * U) {
                 double v[U];
                 size_t dst[U];
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32
                         const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
                         if (lo >= clo && lo < chi) {
                             dst[u] = hi + (size_t)lo * ld;
-                            v[u] = (wup && j < ndo && i >= ndo) ? Fc[(ec + j) + (size_t)(ec + i) * fc] : colc[i];
+                            v[u] = (wup && j < ndo && i >= ndo) ? Fc[(ec + j) + (size_t)(ec + i) * ldc] : colc[i];
                         }
                     }
                 }
@@ -251,6 +252,15 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32_t* __restrict__ list, int S) {
+    assemble_front(P, list, S, 0);
+}
+
+// restore of fronts whose fast-path pass failed: the same assembly, flagged fronts only
+__global__ void __launch_bounds__(kAsmThreads) k_reassemble(DevPlan P, const int32_t* __restrict__ list, int S) {
+    assemble_front(P, list, S, 1);
 }
 
 // ---------------------------------------------------------------- a3 + a4 + a5 (reference)
@@ -287,7 +297,7 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
     }
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
     const bool root = (c == 0);
     const double u = P.u;
     const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
@@ -469,7 +479,8 @@ void launch_assemble(const DevPlan& P, const int32_t* fronts, int nfronts, int b
     // CTAs per front: enough to give ~4 resident CTAs per SM on the whole level
     int S = (int)((4 * 148 + (int64_t)nfronts * batch - 1) / ((int64_t)nfronts * batch));
     S = std::max(1, std::min(S, 16));
-    k_assemble<<<dim3(nfronts * S, batch), kAsmThreads, 0, st>>>(P, fronts, S, only_flagged ? 1 : 0);
+    if (only_flagged) k_reassemble<<<dim3(nfronts * S, batch), kAsmThreads, 0, st>>>(P, fronts, S);
+    else k_assemble<<<dim3(nfronts * S, batch), kAsmThreads, 0, st>>>(P, fronts, S);
 }
 
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,

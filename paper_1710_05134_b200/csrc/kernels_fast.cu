@@ -33,6 +33,11 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
     const int sz = valid ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(sz));
 }
+// 16-byte copy (two doubles), `bytes` in {0, 8, 16} valid source bytes, the rest zero-filled
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int bytes) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -40,8 +45,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restrict__ items) {
     // CB -= L21 D L21^T = G S G^T: both operands are rows of G (upper part, written by
     // k_l21), S = diag(+-1) applied to the B fragments as sign-bit flips (no FP64 work).
-    __shared__ __align__(16) double As[2][KC][APAD];
-    __shared__ __align__(16) double Bs[2][ST][BPAD];
+    __shared__ __align__(16) double As[2][ST][BPAD];      // [row][t]: G rows of the tile's CB rows
+    __shared__ __align__(16) double Bs[2][ST][BPAD];      // [col][t]: G rows of the tile's CB columns
     __shared__ unsigned long long Sg[2][KC];
     const int4 it = items[blockIdx.x];          // (front, I, J, -)
     const int s = it.x, I = it.y, J = it.z;
@@ -51,7 +56,7 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
     if (P.flag[(size_t)sh * P.nf + s] != FL_OK) return;   // redone by the unblocked kernel (CB updated there)
     const int ndo = P.nd_out[(size_t)sh * P.nf + s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
     const int e = q - ndo;                       // eliminated pivots = K
     if (e <= 0) return;
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
@@ -61,19 +66,17 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
     const int g = lane >> 2, tg = lane & 3;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
     auto load = [&](int buf, int t0) {
-        for (int x = tid; x < KC * ST; x += SCH_T) {
-            const int i = x / KC, tt = x - i * KC;
-            const int gi = r0 + i, gt = t0 + tt;
-            const bool v = gi < f && gt < e;
-            cp_async8(&As[buf][tt][i], F + (v ? (gt + (size_t)gi * ld) : 0), v);
+        // rows are 16-byte aligned (even leading dimension): one 16-byte copy per pair of pivots
+        for (int x = tid; x < ST * (KC / 2); x += SCH_T) {
+            const int i = x / (KC / 2), tt = 2 * (x - i * (KC / 2));
+            const int gt = t0 + tt;
+            const int gi = r0 + i, gj = c0 + i;
+            const int nv = gt + 1 < e ? 16 : (gt < e ? 8 : 0);
+            const int na = gi < f ? nv : 0, nb = gj < f ? nv : 0;
+            cp_async16(&As[buf][i][tt], F + (na ? (gt + (size_t)gi * ld) : 0), na);
+            cp_async16(&Bs[buf][i][tt], F + (nb ? (gt + (size_t)gj * ld) : 0), nb);
         }
         if (tid < KC) Sg[buf][tid] = (t0 + tid < e && A.sgn[t0 + tid] < 0.0) ? 0x8000000000000000ull : 0ull;
-        for (int x = tid; x < KC * ST; x += SCH_T) {
-            const int jj = x / KC, t = x % KC;
-            const int gj = c0 + jj, gt = t0 + t;
-            const bool v = gj < f && gt < e;
-            cp_async8(&Bs[buf][jj][t], F + (v ? (gt + (size_t)gj * ld) : 0), v);
-        }
         cp_async_commit();
     };
     double acc[4][4][2];
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
         for (int k4 = 0; k4 < KC; k4 += 4) {
             double a[4], b[4];
 #pragma unroll
-            for (int mb = 0; mb < 4; ++mb) a[mb] = As[buf][k4 + tg][wm + 8 * mb + g];
+            for (int mb = 0; mb < 4; ++mb) a[mb] = As[buf][wm + 8 * mb + g][k4 + tg];
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb)
                 b[nb] = __longlong_as_double(__double_as_longlong(Bs[buf][wn + 8 * nb + g][k4 + tg]) ^ (long long)Sg[buf][k4 + tg]);
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(SS_T) k_schur_small(DevPlan P, const int32_t* 
     if (P.flag[(size_t)sh * P.nf + s] != FL_OK) return;
     const int ndo = P.nd_out[(size_t)sh * P.nf + s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
     const int e = q - ndo;
     if (e <= 0 || c <= 0) return;
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];

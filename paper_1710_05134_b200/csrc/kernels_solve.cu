@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const in
     const int s = fronts[blockIdx.x];
     const int nd = P.nd_in[s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = f;
+    const int f = P.forder[s] + nd, q = p + nd, ldf = ldpad(f), ld = f;     // ldf: front, ld: stored panel
     const int e = q - P.nd_out[s];
     const int flag = P.flag[s];
     const double* F = P.arena + P.arena_off[s];
@@ -76,12 +76,12 @@ __global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const in
         for (int i = threadIdx.x; i < f; i += ST_T) {
             double v = 0.0;
             if (i > t && !(kd == PK_2X2A && i == t + 1)) {
-                if (flag == FL_REF) v = F[i + (size_t)t * ld];
+                if (flag == FL_REF) v = F[i + (size_t)t * ldf];
                 else if (i < q) {      // fast path FS rows hold B' = L11 D M^-T (k_prep): L11 = B' (D M^-T)^-1
-                    if (kd == PK_2X2A) v = F[i + (size_t)t * ld] * A.gca[t] + F[i + (size_t)(t + 1) * ld] * A.gcb[t + 1];
-                    else if (kd == PK_2X2B) v = F[i + (size_t)t * ld] * A.gca[t] + F[i + (size_t)(t - 1) * ld] * A.gcb[t - 1];
-                    else v = F[i + (size_t)t * ld] * A.gca[t];
-                } else v = F[t + (size_t)i * ld] * ca + (o ? F[(t + o) + (size_t)i * ld] * cb : 0.0);
+                    if (kd == PK_2X2A) v = F[i + (size_t)t * ldf] * A.gca[t] + F[i + (size_t)(t + 1) * ldf] * A.gcb[t + 1];
+                    else if (kd == PK_2X2B) v = F[i + (size_t)t * ldf] * A.gca[t] + F[i + (size_t)(t - 1) * ldf] * A.gcb[t - 1];
+                    else v = F[i + (size_t)t * ldf] * A.gca[t];
+                } else v = F[t + (size_t)i * ldf] * ca + (o ? F[(t + o) + (size_t)i * ldf] * cb : 0.0);
             }
             if (kd == PK_ZERO) v = 0.0;
             col[i] = v;

@@ -48,7 +48,8 @@ void plan_memory(Symbolic& S, int slack) {
     for (int64_t s = 0; s < nf; ++s) {
         int64_t cap = (int64_t)S.forder[s] + slack;
         S.capacity[s] = (int32_t)cap;
-        need[s] = ((cap * cap + 31) / 32) * 32;       // 256-byte aligned blocks
+        const int64_t ldc = (cap + 1) & ~int64_t(1);  // fronts use an even leading dimension (ldpad)
+        need[s] = ((ldc * cap + 31) / 32) * 32;       // 256-byte aligned blocks
     }
     std::map<int64_t, int64_t> freel;                 // offset -> size
     int64_t top = 0;
