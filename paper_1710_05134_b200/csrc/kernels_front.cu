@@ -115,6 +115,10 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
     const int sz = valid ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(sz));
 }
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int bytes) {   // bytes in {0, 8, 16}
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -617,13 +621,13 @@ __global__ void __launch_bounds__(FT) k_prep(DevPlan P, const int32_t* __restric
 // is the fully updated CB part of the delayed column).
 __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict__ items) {
     extern __shared__ __align__(16) double l21_smem[];
-    double (*As)[KC][APAD] = reinterpret_cast<double (*)[KC][APAD]>(l21_smem);                   // [LST][KC][APAD]
-    double (*Bs)[LB][BP] = reinterpret_cast<double (*)[LB][BP]>(l21_smem + LST * KC * APAD);      // [LST][LB][BP]
-    double (*Sbase)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * KC * APAD + LST * LB * BP);
-    static_assert(LR * (LB + 1) <= LST * KC * APAD, "Sacc aliases As");
+    double (*As)[LR][BP] = reinterpret_cast<double (*)[LR][BP]>(l21_smem);                       // [LST][LR][BP] rows x t
+    double (*Bs)[LB][BP] = reinterpret_cast<double (*)[LB][BP]>(l21_smem + LST * LR * BP);        // [LST][LB][BP]
+    double (*Sbase)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * LR * BP + LST * LB * BP);
+    static_assert(LR * (LB + 1) <= LST * LR * BP, "Sacc aliases As");
     static_assert(LB * (LB + 1) <= LST * LB * BP, "Lbb aliases Bs");
     double (*Sacc)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem);
-    double (*Lbb)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * KC * APAD);
+    double (*Lbb)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * LR * BP);
     __shared__ int sperm[LB];
     __shared__ int skind[LB];                             // pivot kind of the block columns (-1: delayed / none)
     __shared__ double sgca[LB], sgcb[LB];
@@ -675,11 +679,11 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
             for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
         if (K > 0) {
             auto load = [&](int buf, int t0) {
-                for (int x = tid; x < KC * LR; x += LT) {
-                    const int ii = x / KC, tt = x - ii * KC;
+                for (int x = tid; x < (KC / 2) * LR; x += LT) {   // G rows: 16-byte pairs (even ld, t0 % 16 == 0)
+                    const int ii = x / (KC / 2), tt = 2 * (x - ii * (KC / 2));
                     const int gi = r0 + ii, gt = t0 + tt;
-                    const bool v = gi < f && gt < K;
-                    cp_async8(&As[buf][tt][ii], F + (v ? (gt + (size_t)gi * ld) : 0), v);
+                    const int nb = gi < f ? (gt + 1 < K ? 16 : (gt < K ? 8 : 0)) : 0;
+                    cp_async16(&As[buf][ii][tt], F + (nb ? (gt + (size_t)gi * ld) : 0), nb);
                 }
                 for (int x = tid; x < KC * LB; x += LT) {
                     const int tt = x / LB, jj = x - tt * LB;
@@ -708,7 +712,7 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
                 for (int k4 = 0; k4 < KC; k4 += 4) {
                     double a[2], b[4];
 #pragma unroll
-                    for (int mb = 0; mb < 2; ++mb) a[mb] = As[buf][k4 + tg][wm + 8 * mb + g];
+                    for (int mb = 0; mb < 2; ++mb) a[mb] = As[buf][wm + 8 * mb + g][k4 + tg];
 #pragma unroll
                     for (int nb = 0; nb < 4; ++nb) b[nb] = Bs[buf][8 * nb + g][k4 + tg];
 #pragma unroll
@@ -978,7 +982,7 @@ void launch_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch
 
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
     if (nitems <= 0) return;
-    const size_t smem = sizeof(double) * (LST * KC * APAD + LST * LB * BP + LR * (LB + 1));
+    const size_t smem = sizeof(double) * (LST * LR * BP + LST * LB * BP + LR * (LB + 1));
     static bool attr = false;
     if (!attr) { cudaFuncSetAttribute(k_l21, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
     k_l21<<<dim3(nitems, batch), LT, smem, st>>>(P, items);
