@@ -513,10 +513,6 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                             c->prof.launches[KEP_K_FSU]++;
                         }
                     }
-                    mark(KEP_K_L21, true);
-                    kep::launch_prep(P, fl, nfl2, m, c->stream);            // L11 -> B' = L11 D M^-T (every fast front)
-                    mark(KEP_K_L21, false);
-                    c->prof.launches[KEP_K_L21]++;
                     if (c->litem_cnt[L]) {
                         mark(KEP_K_L21, true);
                         kep::launch_l21(P, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, c->stream);

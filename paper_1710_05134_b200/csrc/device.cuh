@@ -62,8 +62,8 @@ struct DevPlan {
 
 // pivot kinds recorded per eliminated position
 constexpr int PK_1X1 = 0, PK_2X2A = 1, PK_2X2B = 2, PK_ZERO = 3;
-constexpr int AUX_W = 13;        // doubles per position: diag backup, d, ds, fa, fb, cm, (kind, perm), (step, label),
-                                 // sgn, gca, gcb, hca, hcb
+constexpr int AUX_W = 11;        // doubles per position: diag backup, d, ds, fa, fb, cm, (kind, perm), (step, label),
+                                 // sgn, gca, gcb
 // front states: FL_OK = factorised, FL_REF = hand to the unblocked kernel,
 // FL_RERUN = rerun the fast path with one more forced delay, FL_ACTIVE = in the current fast pass
 constexpr int FL_OK = 0, FL_REF = 1, FL_RERUN = 2, FL_ACTIVE = 3;
@@ -77,7 +77,6 @@ struct AuxRec {
     int* label;                  // assembly-order variable (elimination position) of each FS position
     double* sgn;                 // +-1: sign of the eigenvalue of D carried by the G column (k_schur)
     double *gca, *gcb;           // G[:, t] = W21[:, t] gca[t] + W21[:, t +- 1] gcb[t] (2x2 partner)
-    double *hca, *hcb;           // (L11 D M^-T)[:, t] = L11[:, t] hca[t] + L11[:, t +- 1] hcb[t], so G B'^T = W21 L11^T
 };
 
 __device__ __forceinline__ AuxRec aux_rec(const DevPlan& P, int sh, int s, int Q) {
@@ -92,8 +91,6 @@ __device__ __forceinline__ AuxRec aux_rec(const DevPlan& P, int sh, int s, int Q
     A.sgn = b + 8 * Q;
     A.gca = b + 9 * Q;
     A.gcb = b + 10 * Q;
-    A.hca = b + 11 * Q;
-    A.hcb = b + 12 * Q;
     return A;
 }
 
@@ -159,7 +156,6 @@ void launch_combine(const double* V, int64_t ldv, int j, const double* c, double
 void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const double* r, const double* g, int m,
                  double* X, int64_t ldx, int64_t n, cudaStream_t st);
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
-void launch_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 int front_nb_for(int qmax, int64_t nblocks = 0);   // block width (0: too large, use the reference kernel)
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);

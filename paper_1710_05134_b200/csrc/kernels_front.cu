@@ -461,13 +461,12 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
                 step++;
             }
         }
-        // ---- commit the block: L (FS rows), D and the test record; FS trailing update
+        // ---- commit the block: G11 = L11 M (FS rows), D and the test record (k_fsu: FS trailing update)
         const int nbn = e - kp;
+        __syncthreads();                                     // the S1 loop is done with cs / co
         for (int t = warp; t < nbn; t += TH / 32) {
             const int cpos = kp + t;
             const int o = S.oo[t];
-            const int i1 = cpos + 1 + (o == 1 ? 1 : 0);
-            for (int i = i1 + lane; i < q; i += 32) F[i + (size_t)cpos * ld] = S.Ls[(size_t)t * RS + (i - kp)];
             if (lane == 0) {
                 F[cpos + (size_t)cpos * ld] = S.d1[t];
                 if (o == 1) F[cpos + 1 + (size_t)cpos * ld] = 0.0;      // unit L: D's 2x2 coupling is in the record
@@ -482,8 +481,8 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
                     A.sgn[cpos] = sg;
                     A.gca[cpos] = S.tp[t] == PK_ZERO ? 0.0 : sg / sqrt(fabs(dd));
                     A.gcb[cpos] = 0.0;
-                    A.hca[cpos] = S.tp[t] == PK_ZERO ? 0.0 : sg * sqrt(fabs(dd));   // d / sqrt|d|
-                    A.hcb[cpos] = 0.0;
+                    S.cs[t] = S.tp[t] == PK_ZERO ? 0.0 : sqrt(fabs(dd));             // G = L sqrt|d|
+                    S.co[t] = 0.0;
                 } else if (o == 1) {                                // 2x2: G = W Q |Lambda|^-1/2 S
                     double cs, sn, l1, l2;
                     pair_eig(S.d1[t], S.d2[t], S.d1[t + 1], cs, sn, l1, l2);
@@ -493,11 +492,21 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
                     A.sgn[cpos + 1] = s2;
                     A.gca[cpos] = cs * k1;      A.gcb[cpos] = sn * k1;        // G_t   = (W_t cs + W_t+1 sn) k1
                     A.gca[cpos + 1] = cs * k2;  A.gcb[cpos + 1] = -sn * k2;   // G_t+1 = (W_t+1 cs - W_t sn) k2
-                    const double h1 = s1 * sqrt(fabs(l1)), h2 = s2 * sqrt(fabs(l2));   // D M^-T = Q S |Lambda|^1/2
-                    A.hca[cpos] = cs * h1;      A.hcb[cpos] = sn * h1;        // B'_t   = L_t cs h1 + L_t+1 sn h1
-                    A.hca[cpos + 1] = cs * h2;  A.hcb[cpos + 1] = -sn * h2;   // B'_t+1 = L_t+1 cs h2 - L_t sn h2
+                    const double r1 = sqrt(fabs(l1)), r2 = sqrt(fabs(l2));   // G = L M, M = Q |Lambda|^1/2
+                    S.cs[t] = cs * r1;          S.co[t] = sn * r1;
+                    S.cs[t + 1] = cs * r2;      S.co[t + 1] = -sn * r2;
                 }
             }
+        }
+        __syncthreads();
+        for (int t = warp; t < nbn; t += TH / 32) {
+            const int cpos = kp + t;
+            const int o = S.oo[t];
+            const int i1 = cpos + 1 + (o == 1 ? 1 : 0);
+            const double* Lt = S.Ls + (size_t)t * RS - kp;
+            const double* Lo = S.Ls + (size_t)(t + o) * RS - kp;
+            const double ca = S.cs[t], cb = S.co[t];
+            for (int i = i1 + lane; i < q; i += 32) F[i + (size_t)cpos * ld] = Lt[i] * ca + (o ? Lo[i] * cb : 0.0);
         }
         __syncthreads();
     }
@@ -509,8 +518,8 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
 
 
 // ------------------------------------------------------------------ k_fsu
-// FS x FS trailing block [e, q)^2 (lower) -= L[:, kp:e] W[:, kp:e]^T after the
-// block [kp, e) committed by k_fsp, W = L D formed from the pivot record.
+// FS x FS trailing block [e, q)^2 (lower) -= L D L^T over the block [kp, e)
+// committed by k_fsp = G S G^T with G = L M (stored), S = diag(+-1).
 // One CTA per 64 x 64 tile (tiles anchored at the current e).
 constexpr int UT = 128;
 constexpr int UK = 32;          // >= any NB
@@ -543,13 +552,7 @@ __global__ void __launch_bounds__(UT) k_fsu(DevPlan P, const int4* __restrict__ 
         const int gi = i0 + ii, gj = j0 + ii;
         As[t][ii] = (vt && gi < q) ? F[gi + (size_t)(kp + t) * ld] : 0.0;
         double w = 0.0;
-        if (vt && gj < q) {
-            const int pos = kp + t, kd = A.kind[pos];
-            const double* Lj = F + gj;
-            if (kd == PK_1X1) w = Lj[(size_t)pos * ld] * A.d[pos];
-            else if (kd == PK_2X2A) w = Lj[(size_t)pos * ld] * A.d[pos] + Lj[(size_t)(pos + 1) * ld] * A.ds[pos];
-            else if (kd == PK_2X2B) w = Lj[(size_t)(pos - 1) * ld] * A.ds[pos - 1] + Lj[(size_t)pos * ld] * A.d[pos];
-        }
+        if (vt && gj < q) w = F[gj + (size_t)(kp + t) * ld] * A.sgn[kp + t];    // (G S)[j, t]
         Bs[ii][t] = w;
     }
     __syncthreads();
@@ -582,39 +585,6 @@ __global__ void __launch_bounds__(UT) k_fsu(DevPlan P, const int4* __restrict__ 
             }
 }
 
-// ------------------------------------------------------------------ k_prep
-// After the FS factorisation of a front: L11 -> B' = L11 D M^-T in place (rows below
-// each pivot block), so that W21 L11^T = G B'^T with G = W21 D^-1 M (k_l21, k_schur).
-__global__ void __launch_bounds__(FT) k_prep(DevPlan P, const int32_t* __restrict__ fronts) {
-    const int s = fronts[blockIdx.x];
-    const int sh = blockIdx.y;
-    if (P.flag[(size_t)sh * P.nf + s] != FL_ACTIVE) return;
-    const int nd = P.nd_in[(size_t)sh * P.nf + s];
-    const int p = P.npiv[s], c = P.ncb[s];
-    const int q = p + nd, ld = ldpad(P.forder[s] + nd);
-    const int e = q - P.nd_out[(size_t)sh * P.nf + s];
-    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
-    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int t = warp; t < e; t += FT / 32) {
-        const int kd = A.kind[t];
-        if (kd == PK_2X2B) continue;                    // handled with its first column
-        double* c0 = F + (size_t)t * ld;
-        if (kd == PK_2X2A) {
-            double* c1 = c0 + ld;
-            const double a0 = A.hca[t], b0 = A.hcb[t], a1 = A.hca[t + 1], b1 = A.hcb[t + 1];
-            for (int j = t + 2 + lane; j < q; j += 32) {
-                const double l0 = c0[j], l1 = c1[j];
-                c0[j] = l0 * a0 + l1 * b0;
-                c1[j] = l1 * a1 + l0 * b1;
-            }
-        } else {
-            const double a0 = A.hca[t];
-            for (int j = t + 1 + lane; j < q; j += 32) c0[j] *= a0;
-        }
-    }
-}
-
 // ------------------------------------------------------------------ k_l21
 // W21 = A21 P^T L11^-T for 64 CB rows of one front; column maxima of W21.
 // L11[i,t] = 0 for t >= e (delayed columns have no pivot: their W21 column
@@ -629,6 +599,7 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
     double (*Sacc)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem);
     double (*Lbb)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * LR * BP);
     __shared__ int sperm[LB];
+    __shared__ unsigned long long SgB[LST][KC];          // sign bits of B' = G11 S for the K chunks
     __shared__ int skind[LB];                             // pivot kind of the block columns (-1: delayed / none)
     __shared__ double sgca[LB], sgcb[LB];
     const int4 it = items[blockIdx.x];
@@ -691,6 +662,7 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
                     const bool v = jj < nbc && gt < K;
                     cp_async8(&Bs[buf][jj][tt], F + (v ? ((b0 + jj) + (size_t)gt * ld) : 0), v);
                 }
+                if (tid < KC) SgB[buf][tid] = (t0 + tid < K && A.sgn[t0 + tid] < 0.0) ? 0x8000000000000000ull : 0ull;
                 cp_async_commit();
             };
             const int nk = (K + KC - 1) / KC;
@@ -714,7 +686,8 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
 #pragma unroll
                     for (int mb = 0; mb < 2; ++mb) a[mb] = As[buf][wm + 8 * mb + g][k4 + tg];
 #pragma unroll
-                    for (int nb = 0; nb < 4; ++nb) b[nb] = Bs[buf][8 * nb + g][k4 + tg];
+                    for (int nb = 0; nb < 4; ++nb)
+                        b[nb] = __longlong_as_double(__double_as_longlong(Bs[buf][8 * nb + g][k4 + tg]) ^ (long long)SgB[buf][k4 + tg]);
 #pragma unroll
                     for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
@@ -733,11 +706,11 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
             for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) Sacc[wm + 8 * mb + g][8 * nb + 2 * tg + h] = acc[mb][nb][h];
-        // diagonal block of B' = L11 D M^-T (strict lower, columns < e only; k_prep)
+        // diagonal block of B' = L11 D M^-T = G11 S (strict lower, columns < e only)
         for (int x = tid; x < LB * LB; x += LT) {           // consecutive threads walk a column (coalesced)
             const int b = x / LB, a = x - b * LB;
             double v = 0.0;
-            if (a < nbc && b < a && b0 + b < e) v = F[(b0 + a) + (size_t)(b0 + b) * ld];
+            if (a < nbc && b < a && b0 + b < e) v = F[(b0 + a) + (size_t)(b0 + b) * ld] * A.sgn[b0 + b];   // B' = G S
             Lbb[a][b] = v;
         }
         __syncthreads();
@@ -973,11 +946,6 @@ void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch,
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
     if (nitems <= 0) return;
     k_fsu<<<dim3(nitems, batch), UT, 0, st>>>(P, items);
-}
-
-void launch_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
-    if (nfronts <= 0) return;
-    k_prep<<<dim3(nfronts, batch), FT, 0, st>>>(P, fronts);
 }
 
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {

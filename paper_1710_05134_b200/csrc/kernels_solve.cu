@@ -77,10 +77,11 @@ __global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const in
             double v = 0.0;
             if (i > t && !(kd == PK_2X2A && i == t + 1)) {
                 if (flag == FL_REF) v = F[i + (size_t)t * ldf];
-                else if (i < q) {      // fast path FS rows hold B' = L11 D M^-T (k_prep): L11 = B' (D M^-T)^-1
-                    if (kd == PK_2X2A) v = F[i + (size_t)t * ldf] * A.gca[t] + F[i + (size_t)(t + 1) * ldf] * A.gcb[t + 1];
-                    else if (kd == PK_2X2B) v = F[i + (size_t)t * ldf] * A.gca[t] + F[i + (size_t)(t - 1) * ldf] * A.gcb[t - 1];
-                    else v = F[i + (size_t)t * ldf] * A.gca[t];
+                else if (i < q) {      // fast path FS rows hold G11 = L11 M (k_fsp): B' = G11 S, L11 = B' (D M^-T)^-1
+                    const double bt = F[i + (size_t)t * ldf] * A.sgn[t];
+                    if (kd == PK_2X2A) v = bt * A.gca[t] + F[i + (size_t)(t + 1) * ldf] * A.sgn[t + 1] * A.gcb[t + 1];
+                    else if (kd == PK_2X2B) v = bt * A.gca[t] + F[i + (size_t)(t - 1) * ldf] * A.sgn[t - 1] * A.gcb[t - 1];
+                    else v = bt * A.gca[t];
                 } else v = F[t + (size_t)i * ldf] * ca + (o ? F[(t + o) + (size_t)i * ldf] * cb : 0.0);
             }
             if (kd == PK_ZERO) v = 0.0;
