@@ -47,6 +47,7 @@ struct kep_ctx {
     int64_t csr_nnz = 0;
     int64_t *d_arena_off = nullptr, *d_asm_ptr = nullptr, *d_asm_src = nullptr, *d_rmap_ptr = nullptr;
     uint32_t* d_asm_rc = nullptr;
+    int32_t* d_asm_col = nullptr;
     int32_t* d_rmap = nullptr;
     double *d_a = nullptr, *d_b = nullptr;
     // batch state
@@ -61,6 +62,15 @@ struct kep_ctx {
     int32_t* d_lists = nullptr;                 // [fast fronts of all levels | ref fronts of all levels]
     int4* d_items = nullptr;                    // Schur tiles (front, I, J, 0)
     int4* d_litems = nullptr;                   // k_l21 row tiles (front, I, 0, 0)
+    int4* d_lsitems = nullptr;                  // k_l21<1> row tiles (fronts with q < 32)
+    int4* d_lxitems = nullptr;                  // k_l21<2> row tiles (GEMM in-block solve)
+    int32_t* d_xfronts = nullptr;               // k_l21x_prep fronts per level
+    int64_t* d_xoff = nullptr;                  // X scratch offsets (within the level)
+    double* d_xscr = nullptr;
+    int64_t xstride = 0;
+    std::vector<int64_t> lsitem_off, lsitem_cnt, lxitem_off, lxitem_cnt, xfront_off, xfront_cnt;
+    int4* d_aitems = nullptr;                   // k_assemble strips (front, x, S, 0): all fronts, then fast fronts
+    std::vector<int64_t> aitem_off, aitem_cnt, raitem_off, raitem_cnt;
     std::vector<int64_t> fast_off, fast_cnt, ref_off, ref_cnt, item_off, item_cnt, litem_off, litem_cnt;
     // fast-path pivot records: per-front offsets (entries), per shift stride (doubles)
     int64_t* d_aux_off = nullptr;
@@ -151,6 +161,7 @@ void free_batch(kep_ctx* c) {
     cudaFree(c->d_forced); c->d_forced = nullptr;
     cudaFree(c->d_fstate); c->d_fstate = nullptr;
     cudaFree(c->d_gscratch); c->d_gscratch = nullptr;
+    cudaFree(c->d_xscr); c->d_xscr = nullptr;
     cudaFree(c->d_pending); c->d_pending = nullptr;
 }
 
@@ -159,7 +170,8 @@ kep_status alloc_batch(kep_ctx* c) {
     free_batch(c);
     size_t freeb = 0, totalb = 0;
     KEP_CUDA(c, cudaMemGetInfo(&freeb, &totalb));
-    const size_t per_shift = ((size_t)c->sym.arena_doubles + (size_t)c->aux_stride + (size_t)c->gscratch_stride) * sizeof(double);
+    const size_t per_shift =
+        ((size_t)c->sym.arena_doubles + (size_t)c->aux_stride + (size_t)c->gscratch_stride + (size_t)c->xstride) * sizeof(double);
     int cap = std::max(1, c->opts.max_batch);
     const size_t budget = (size_t)(0.85 * (double)freeb);
     while (cap > 1 && per_shift * (size_t)cap > budget) cap--;
@@ -180,6 +192,7 @@ kep_status alloc_batch(kep_ctx* c) {
     KEP_CUDA(c, cudaMalloc(&c->d_forced, nfb * (kep::FMAX + 1)));
     KEP_CUDA(c, cudaMalloc(&c->d_fstate, nfb * kep::FSTATE_W));
     KEP_CUDA(c, cudaMalloc(&c->d_gscratch, sizeof(double) * std::max<int64_t>(c->gscratch_stride, 1) * cap));
+    KEP_CUDA(c, cudaMalloc(&c->d_xscr, sizeof(double) * std::max<int64_t>(c->xstride, 1) * cap));
     KEP_CUDA(c, cudaMalloc(&c->d_pending, 2 * sizeof(int32_t)));
     c->h_stats.resize(cap);
     return KEP_OK;
@@ -192,9 +205,23 @@ kep_status build_lists(kep_ctx* c) {
     const int nl = (int)S.level_ptr.size() - 1;
     const bool use_fast = c->opts.kernel_variant == 0;
     std::vector<int32_t> fast, ref;
-    std::vector<int4> items, litems, uitems;
+    std::vector<int4> items, litems, lsitems, lxitems, uitems;
+    std::vector<int32_t> xfronts;
+    std::vector<int64_t> xoff(S.nf > 0 ? S.nf : 1, 0);
+    int64_t xmax = 0;
     std::vector<int32_t> small;
     c->litem_off.assign(nl, 0); c->litem_cnt.assign(nl, 0);
+    c->lsitem_off.assign(nl, 0); c->lsitem_cnt.assign(nl, 0);
+    c->lxitem_off.assign(nl, 0); c->lxitem_cnt.assign(nl, 0);
+    c->xfront_off.assign(nl, 0); c->xfront_cnt.assign(nl, 0);
+    c->aitem_off.assign(nl, 0); c->aitem_cnt.assign(nl, 0);
+    c->raitem_off.assign(nl, 0); c->raitem_cnt.assign(nl, 0);
+    std::vector<int4> aitems;
+    auto strips = [&](int s, int rmax) {              // rmax: CTAs per front (k_reassemble loops)
+        const int ns = kep::assembly_strips((int)S.forder[s]);
+        const int r = std::min(ns, rmax);
+        for (int x = 0; x < r; ++x) aitems.push_back(make_int4(s, x, ns, r));
+    };
     c->uitem_off.assign(nl, 0); c->uitem_cnt.assign(nl, 0);
     c->small_off.assign(nl, 0); c->small_cnt.assign(nl, 0);
     c->fast_off.assign(nl, 0); c->fast_cnt.assign(nl, 0);
@@ -206,15 +233,34 @@ kep_status build_lists(kep_ctx* c) {
         c->ref_off[L] = (int64_t)ref.size();
         c->item_off[L] = (int64_t)items.size();
         c->litem_off[L] = (int64_t)litems.size();
+        c->lsitem_off[L] = (int64_t)lsitems.size();
+        c->lxitem_off[L] = (int64_t)lxitems.size();
+        c->xfront_off[L] = (int64_t)xfronts.size();
+        int64_t xacc = 0;
         c->uitem_off[L] = (int64_t)uitems.size();
         c->small_off[L] = (int64_t)small.size();
+        c->aitem_off[L] = (int64_t)aitems.size();
+        for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) strips(S.level_fronts[k], INT_MAX);
+        c->aitem_cnt[L] = (int64_t)aitems.size() - c->aitem_off[L];
+        c->raitem_off[L] = (int64_t)aitems.size();
+        for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k)
+            if (use_fast && kep::front_nb_for(S.capacity[S.level_fronts[k]] - S.ncb[S.level_fronts[k]]) > 0)
+                strips(S.level_fronts[k], 8);
+        c->raitem_cnt[L] = (int64_t)aitems.size() - c->raitem_off[L];
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
             const int s = S.level_fronts[k];
             const int qcap = S.capacity[s] - S.ncb[s];            // p + slack
             if (use_fast && kep::front_nb_for(qcap) > 0) {
                 fast.push_back(s);
                 c->level_qmax[L] = std::max(c->level_qmax[L], qcap);
-                for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) litems.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
+                const int lmode = kep::l21_mode(qcap);
+                auto& li = lmode == 1 ? lsitems : (lmode == 2 ? lxitems : litems);
+                if (lmode == 2) {
+                    xfronts.push_back(s);
+                    xoff[s] = xacc;
+                    xacc += kep::l21_x_doubles(qcap);
+                }
+                for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) li.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
                 for (int I = 0; I < (qcap + 63) / 64; ++I)
                     for (int J = 0; J <= I; ++J) uitems.push_back(make_int4(s, I, J, 0));
                 if (kep::schur_small_ok(S.ncb[s], qcap)) {
@@ -232,6 +278,10 @@ kep_status build_lists(kep_ctx* c) {
         c->ref_cnt[L] = (int64_t)ref.size() - c->ref_off[L];
         c->item_cnt[L] = (int64_t)items.size() - c->item_off[L];
         c->litem_cnt[L] = (int64_t)litems.size() - c->litem_off[L];
+        c->lsitem_cnt[L] = (int64_t)lsitems.size() - c->lsitem_off[L];
+        c->lxitem_cnt[L] = (int64_t)lxitems.size() - c->lxitem_off[L];
+        c->xfront_cnt[L] = (int64_t)xfronts.size() - c->xfront_off[L];
+        xmax = std::max(xmax, xacc);
         c->uitem_cnt[L] = (int64_t)uitems.size() - c->uitem_off[L];
         c->small_cnt[L] = (int64_t)small.size() - c->small_off[L];
     }
@@ -254,6 +304,17 @@ kep_status build_lists(kep_ctx* c) {
     KEP_CUDA(c, upload(&c->d_small, small));
     cudaFree(c->d_aux_off); c->d_aux_off = nullptr;
     KEP_CUDA(c, upload(&c->d_litems, litems));
+    cudaFree(c->d_lsitems); c->d_lsitems = nullptr;
+    KEP_CUDA(c, upload(&c->d_lsitems, lsitems));
+    cudaFree(c->d_lxitems); c->d_lxitems = nullptr;
+    KEP_CUDA(c, upload(&c->d_lxitems, lxitems));
+    cudaFree(c->d_xfronts); c->d_xfronts = nullptr;
+    KEP_CUDA(c, upload(&c->d_xfronts, xfronts));
+    cudaFree(c->d_xoff); c->d_xoff = nullptr;
+    KEP_CUDA(c, upload(&c->d_xoff, xoff));
+    c->xstride = xmax;
+    cudaFree(c->d_aitems); c->d_aitems = nullptr;
+    KEP_CUDA(c, upload(&c->d_aitems, aitems));
     // pivot-record offsets: Q_s = p_s + slack entries per front
     std::vector<int64_t> aoff(S.nf > 0 ? S.nf : 1, 0);
     int64_t acc = 0;
@@ -335,6 +396,17 @@ kep_status upload_plan(kep_ctx* c, const int64_t* colptr, const int32_t* rowidx)
         std::vector<int32_t> cp(S.cb_ptr.begin(), S.cb_ptr.end());
         std::vector<int32_t> cr(S.cb_rows.begin(), S.cb_rows.end());
         KEP_CUDA(c, upload(&c->d_piv_first, pf));
+        std::vector<int32_t> acol;                       // per front: first entry of each local column
+        acol.reserve((size_t)S.n + S.nf);
+        for (int64_t f = 0; f < S.nf; ++f) {
+            const int64_t a0 = S.asm_ptr[f], a1 = S.asm_ptr[f + 1];
+            int64_t k = a0;
+            for (int j = 0; j <= S.npiv[f]; ++j) {
+                while (k < a1 && (int)(S.asm_rc[k] & 0xffffu) < j) ++k;
+                acol.push_back((int32_t)(k - a0));
+            }
+        }
+        KEP_CUDA(c, upload(&c->d_asm_col, acol));
         KEP_CUDA(c, upload(&c->d_cb_ptr, cp));
         KEP_CUDA(c, upload(&c->d_cb_rows, cr));
         KEP_CUDA(c, upload(&c->d_perm, S.perm));
@@ -372,6 +444,7 @@ DevPlan make_plan(kep_ctx* c) {
     P.child_list = c->d_child_list;
     P.level_fronts = c->d_level_fronts;
     P.piv_first = c->d_piv_first;
+    P.asm_col = c->d_asm_col;
     P.cb_ptr = c->d_cb_ptr;
     P.cb_rows = c->d_cb_rows;
     P.arena_off = c->d_arena_off;
@@ -400,6 +473,9 @@ DevPlan make_plan(kep_ctx* c) {
     P.gscratch = c->d_gscratch;
     P.gscratch_stride = c->gscratch_stride;
     P.goff = c->d_goff;
+    P.xscr = c->d_xscr;
+    P.xstride = c->xstride;
+    P.xoff = c->d_xoff;
     P.debug = getenv("KEP_DEBUG") ? 1 : 0;
     return P;
 }
@@ -480,7 +556,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
         for (int L = 0; L < nl; ++L) {
             const int b = S.level_ptr[L], nfl = S.level_ptr[L + 1] - b;
             mark(KEP_K_ASSEMBLE, true);
-            kep::launch_assemble(P, c->d_level_fronts + b, nfl, m, false, c->stream);
+            kep::launch_assemble(P, c->d_aitems + c->aitem_off[L], (int)c->aitem_cnt[L], m, false, c->stream);
             mark(KEP_K_ASSEMBLE, false);
             c->prof.launches[KEP_K_ASSEMBLE]++;
             if (c->fast_cnt[L]) {
@@ -513,15 +589,19 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                             c->prof.launches[KEP_K_FSU]++;
                         }
                     }
-                    if (c->litem_cnt[L]) {
+                    if (c->litem_cnt[L] || c->lsitem_cnt[L] || c->lxitem_cnt[L]) {
                         mark(KEP_K_L21, true);
-                        kep::launch_l21(P, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, c->stream);
+                        kep::launch_l21x_prep(P, c->d_xfronts + c->xfront_off[L], (int)c->xfront_cnt[L], m, c->stream);
+                        kep::launch_l21(P, c->d_lxitems + c->lxitem_off[L], (int)c->lxitem_cnt[L], m, 2, c->stream);
+                        kep::launch_l21(P, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, 0, c->stream);
+                        kep::launch_l21(P, c->d_lsitems + c->lsitem_off[L], (int)c->lsitem_cnt[L], m, 1, c->stream);
                         mark(KEP_K_L21, false);
-                        c->prof.launches[KEP_K_L21] += 1;
+                        c->prof.launches[KEP_K_L21] += 2 * (c->lxitem_cnt[L] > 0) + (c->litem_cnt[L] > 0) + (c->lsitem_cnt[L] > 0);
                     }
                     mark(KEP_K_CHECK, true);
                     kep::launch_check(P, fl, nfl2, m, c->stream);
-                    kep::launch_assemble(P, fl, nfl2, m, true, c->stream);   // restore failed fronts: assemble again
+                    // restore failed fronts: assemble again
+                    kep::launch_assemble(P, c->d_aitems + c->raitem_off[L], (int)c->raitem_cnt[L], m, true, c->stream);
                     mark(KEP_K_CHECK, false);
                     c->prof.launches[KEP_K_CHECK] += 3;
                 }
@@ -1322,7 +1402,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_level_fronts, c->d_arena_off, c->d_asm_ptr, c->d_asm_src, c->d_rmap_ptr,
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
-                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci,
+                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
                         c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);

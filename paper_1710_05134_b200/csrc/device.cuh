@@ -32,6 +32,7 @@ struct DevPlan {
     const int64_t* arena_off;    // doubles, within one shift's arena
     const int64_t* asm_ptr;
     const uint32_t* asm_rc;      // (lrow << 16) | lcol
+    const int32_t* asm_col;      // [piv_first[s] + s + j] first entry of local column j (j <= p), relative to asm_ptr[s]
     const double* a;             // A values in assembly order
     const double* b;             // B values in assembly order
     const int64_t* rmap_ptr;
@@ -57,6 +58,9 @@ struct DevPlan {
     double* gscratch;            // [batch][gscratch_stride] k_fsp block columns of FS blocks too large for smem
     int64_t gscratch_stride;
     const int64_t* goff;         // [nf] scratch offset, -1 = shared memory
+    double* xscr;                // [batch][xstride] k_l21x_prep blocks X = [L_bb^-T | L_bb^-T D^-1 M] (one level)
+    int64_t xstride;
+    const int64_t* xoff;         // [nf] offset in the level's X scratch (k_l21<2> fronts)
     int32_t debug;               // KEP_DEBUG set: diagnostic printf in rare paths
 };
 
@@ -135,8 +139,8 @@ struct StorePlan {
 };
 
 // Launchers (kernels.cu, kernels_front.cu, kernels_fast.cu, kernels_solve.cu)
-void launch_assemble(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, bool only_flagged,
-                     cudaStream_t st);
+void launch_assemble(const DevPlan& P, const int4* items, int nitems, int batch, bool only_flagged, cudaStream_t st);
+int assembly_strips(int forder);     // CTAs (column strips) per front of the given order
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st);
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 int fs_iters(int qmax, int64_t nblocks);   // k_fsp launches that finish every front of a level
@@ -155,7 +159,10 @@ void launch_combine(const double* V, int64_t ldv, int j, const double* c, double
                     double a1, const double* x1, double a2, const double* x2, int64_t n, cudaStream_t st);
 void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const double* r, const double* g, int m,
                  double* X, int64_t ldx, int64_t n, cudaStream_t st);
-void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
+void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, int mode, cudaStream_t st);
+int l21_mode(int qcap);              // 1: one column block (q < 32); 2: GEMM in-block solve (X scratch); 0: triangle
+int64_t l21_x_doubles(int qcap);     // X scratch of one front (k_l21x_prep)
+void launch_l21x_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 int front_nb_for(int qmax, int64_t nblocks = 0);   // block width (0: too large, use the reference kernel)
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);

@@ -93,7 +93,11 @@ __device__ __forceinline__ double symget(const double* F, int ld, int i, int j) 
 
 // ---------------------------------------------------------------- a1 + a2
 constexpr int kAsmThreads = 256;
-constexpr int kAsmMapMax = 8192;          // child CB positions staged in shared memory
+constexpr int kAsmNW = kAsmThreads / 32;
+constexpr int kAsmMapMax = 16384;         // child row positions staged in shared memory (uint16, all children)
+constexpr int kAsmKids = 32;              // children handled by the gather path (one lane each)
+constexpr int kAsmChunk = 128;            // parent rows per warp work chunk
+constexpr int kAsmStripEnt = 32768;       // target lower-triangle entries per CTA (assembly_strips)
 
 // Columns [lo, hi) of a lower triangle of order ld holding the x-th of S equal
 // shares of its entries (column j has ld - j entries).
@@ -110,14 +114,25 @@ __device__ __forceinline__ void tri_split(int ld, int S, int x, int& lo, int& hi
     hi = col_at(x + 1);
 }
 
-// One front of a level, S CTAs per front (blockIdx.x = front * S + x): CTA x
-// owns the parent columns [lo, hi): zero-fill, original entries (alpha a - sigma b),
-// then the children's CB entries landing in those columns, children in order.
-// Each parent entry belongs to one CTA, so the sum order is fixed (deterministic).
-__device__ __forceinline__ void assemble_front(const DevPlan& P, const int32_t* __restrict__ list, int S,
-                                               int only_flagged) {
-    const int s = list[blockIdx.x / S];
-    const int xs = blockIdx.x % S;
+struct AsmKid {                  // one child as seen by the parent's assembly
+    const double* F;             // child front
+    int ldc, ec, ndo, mc;        // leading dimension, first CB/delayed position, delayed count, CB+delayed count
+    int moff;                    // offset of its row positions in s_pos
+    int dof;                     // parent position of its first delayed column
+    int wup;                     // fast-path child: CB rows of its delayed columns in the upper part
+};
+
+// Strip x of S of one front (columns [lo, hi), lower part).  Gather formulation:
+// each warp owns whole parent columns and builds them in chunks of kAsmChunk rows
+// in a private shared-memory buffer -- zero, original entries (alpha a - sigma b),
+// then for each child in order the contiguous run of its CB column that lands in
+// the chunk (child row positions increase with the child row index) -- and writes
+// each chunk once, coalesced.  No atomics and no block barriers on this path;
+// every parent entry is summed in a fixed order.  Entries of the children's
+// delayed columns (rare) are added afterwards with RED adds, children in order.
+// Fronts with more than kAsmKids children or kAsmMapMax child rows take the plain
+// path: zero-fill, stores, RED adds.
+__device__ __forceinline__ void assemble_strip(const DevPlan& P, const int s, const int xs, const int S, int only_flagged) {
     const int sh = blockIdx.y;
     if (only_flagged) {               // re-assembly of fronts whose fast-path pass failed (restore)
         const int fl = P.flag[(size_t)sh * P.nf + s];
@@ -128,139 +143,267 @@ __device__ __forceinline__ void assemble_front(const DevPlan& P, const int32_t* 
     int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
     const int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
     int32_t* doff = P.doff + (size_t)sh * P.nf;
-    __shared__ int s_nd, s_skip;
+    __shared__ int s_nd, s_skip, s_msum, s_anyd;
     __shared__ double s_red[32];
-    __shared__ int s_pos[kAsmMapMax];
+    __shared__ uint16_t s_pos[kAsmMapMax];
+    __shared__ AsmKid s_kid[kAsmKids];
+    extern __shared__ double s_buf[];                          // [kAsmNW][kAsmChunk]
     const int c0 = P.child_ptr[s], c1 = P.child_ptr[s + 1];
-    if (threadIdx.x == 0) {
-        int off = 0, bad = 0;
-        for (int q = c0; q < c1; ++q) {
-            const int c = P.child_list[q];
-            const int no = nd_out[c];
-            if (no < 0) bad = 1;
-            if (xs == 0) doff[c] = off;
-            off += no > 0 ? no : 0;
+    const int nch = c1 - c0;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int p = P.npiv[s];
+    if (warp == 0) {                  // children: delayed counts (prefix), descriptors
+        int off = 0, bad = 0, msum = 0, anyd = 0;
+        for (int q0 = 0; q0 < nch; q0 += 32) {
+            const int q = q0 + lane;
+            int no = 0, mc = 0, c = -1;
+            if (q < nch) {
+                c = P.child_list[c0 + q];
+                no = nd_out[c];
+                if (no < 0) bad = 1;
+            }
+            const int nz = no > 0 ? no : 0;
+            int inc = nz;                                         // inclusive warp prefix of delayed counts
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const int dof = off + inc - nz;
+            if (q < nch) {
+                if (xs == 0) doff[c] = dof;
+                mc = nz + P.ncb[c];
+                if (q < kAsmKids) {
+                    const int fc = P.forder[c] + nd_in[c];
+                    AsmKid k;
+                    k.F = arena + P.arena_off[c];
+                    k.ldc = ldpad(fc);
+                    k.ec = fc - mc;
+                    k.ndo = nz;
+                    k.mc = mc;
+                    k.moff = 0;
+                    k.dof = p + dof;
+                    k.wup = P.flag[(size_t)sh * P.nf + c] == FL_OK && nz > 0;
+                    s_kid[q] = k;
+                }
+            }
+            int minc = mc;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, minc, o);
+                if (lane >= o) minc += y;
+            }
+            if (q < nch && q < kAsmKids) s_kid[q].moff = msum + minc - mc;
+            msum += __shfl_sync(0xffffffffu, minc, 31);
+            off += __shfl_sync(0xffffffffu, inc, 31);
+            anyd |= __any_sync(0xffffffffu, nz > 0);
+            bad = __any_sync(0xffffffffu, bad);
         }
-        const int need = P.forder[s] + off;
-        if (need > P.cap[s]) {
-            bad = 1;
-            if (xs == 0) atomicMax(&st->need_slack, off);
+        if (lane == 0) {
+            const int need = P.forder[s] + off;
+            if (need > P.cap[s]) {
+                bad = 1;
+                if (xs == 0) atomicMax(&st->need_slack, off);
+            }
+            if (bad && xs == 0) atomicOr(&st->flags, FLAG_OVERFLOW);
+            s_skip = bad;
+            s_nd = off;
+            s_msum = (nch <= kAsmKids) ? msum : INT_MAX;
+            s_anyd = anyd;
+            if (xs == 0) nd_in[s] = bad ? -1 : off;
         }
-        if (bad && xs == 0) atomicOr(&st->flags, FLAG_OVERFLOW);
-        s_skip = bad;
-        s_nd = off;
-        if (xs == 0) nd_in[s] = bad ? -1 : off;
     }
     __syncthreads();
     if (s_skip) return;
-    const int nd = s_nd, p = P.npiv[s], fo = P.forder[s] + nd, ld = ldpad(fo);   // order, leading dimension
+    const int nd = s_nd, fo = P.forder[s] + nd, ld = ldpad(fo);   // order, leading dimension
     double* F = arena + P.arena_off[s];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAsmThreads / 32;
     int clo, chi;
     tri_split(fo, S, xs, clo, chi);
+    const bool gather = s_msum <= kAsmMapMax;
     if (xs == 0) {   // labels of the FS positions: own pivots, then each child's delayed variables
         const AuxRec A = aux_rec(P, sh, s, P.cap[s] - P.ncb[s]);
-        for (int i = threadIdx.x; i < p; i += kAsmThreads) A.label[i] = P.piv_first[s] + i;
-        int off = 0;
-        for (int q = c0; q < c1; ++q) {
-            const int c = P.child_list[q];
-            const int ndo = nd_out[c];
-            if (ndo <= 0) continue;
-            const AuxRec C = aux_rec(P, sh, c, P.cap[c] - P.ncb[c]);
-            const int ec = P.npiv[c] + nd_in[c] - ndo;
-            for (int j = threadIdx.x; j < ndo; j += kAsmThreads) A.label[p + off + j] = C.label[C.perm[ec + j]];
-            off += ndo;
+        for (int i = tid; i < p; i += kAsmThreads) A.label[i] = P.piv_first[s] + i;
+        if (s_anyd) {
+            int off = 0;
+            for (int q = c0; q < c1; ++q) {
+                const int c = P.child_list[q];
+                const int ndo = nd_out[c];
+                if (ndo <= 0) continue;
+                const AuxRec C = aux_rec(P, sh, c, P.cap[c] - P.ncb[c]);
+                const int ec = P.npiv[c] + nd_in[c] - ndo;
+                for (int j = tid; j < ndo; j += kAsmThreads) A.label[p + off + j] = C.label[C.perm[ec + j]];
+                off += ndo;
+            }
         }
     }
-    for (int j = clo + warp; j < chi; j += nw)
-        for (int i = j + lane; i < fo; i += 32) F[i + (size_t)j * ld] = 0.0;
-    __syncthreads();
     const double sigma = P.sigma[sh], alpha = P.alpha[sh];
+    const int64_t a0 = P.asm_ptr[s];
+    const int32_t* acol = P.asm_col + P.piv_first[s] + s;
     double mx = 0.0;
-    for (int64_t k = P.asm_ptr[s] + threadIdx.x; k < P.asm_ptr[s + 1]; k += kAsmThreads) {
-        const uint32_t rc = P.asm_rc[k];
-        const int lr = (int)(rc >> 16), lc = (int)(rc & 0xffffu);
-        if (lc < clo || lc >= chi) continue;
-        const int r = lr < p ? lr : lr + nd;
-        const double v = fma(-sigma, P.b[k], alpha * P.a[k]);      // alpha A - sigma B (alpha = 1: A - sigma B)
-        F[r + (size_t)lc * ld] = v;
-        mx = fmax(mx, fabs(v));
+    if (gather) {
+        // parent positions of every child row, all children (one barrier)
+        for (int q = 0; q < nch; ++q) {
+            const AsmKid& k = s_kid[q];
+            const int32_t* __restrict__ rm = P.rmap + P.rmap_ptr[P.child_list[c0 + q]];
+            const int dof = k.dof;
+            for (int x = tid; x < k.mc; x += kAsmThreads) {
+                int v;
+                if (x < k.ndo) v = dof + x;
+                else { const int r = rm[x - k.ndo]; v = r < p ? r : r + nd; }
+                s_pos[k.moff + x] = (uint16_t)v;
+            }
+        }
+        __syncthreads();
+        double* buf = s_buf + warp * kAsmChunk;
+        // lane q < nch tracks child q: jk = its column landing in parent column c, ia = next row
+        for (int c = clo + warp; c < chi; c += kAsmNW) {
+            int jk = -1, ia = 0, mcq = 0, mo = 0;
+            if (lane < nch) {
+                const AsmKid& k = s_kid[lane];
+                mcq = k.mc; mo = k.moff;
+                int lo = k.ndo, hi = k.mc;                        // first non-delayed row with pos >= c
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if ((int)s_pos[mo + mid] < c) lo = mid + 1; else hi = mid;
+                }
+                if (lo < k.mc && (int)s_pos[mo + lo] == c) { jk = lo; ia = lo; }
+            }
+            const int e0 = c < p ? acol[c] : 0, e1 = c < p ? acol[c + 1] : 0;
+            for (int r0 = c; r0 < fo; r0 += kAsmChunk) {
+                const int r1 = min(r0 + kAsmChunk, fo);
+#pragma unroll
+                for (int u = 0; u < kAsmChunk / 32; ++u) buf[lane + 32 * u] = 0.0;
+                __syncwarp();
+                for (int e = e0 + lane; e < e1; e += 32) {        // original entries of column c in [r0, r1)
+                    const uint32_t rc = P.asm_rc[a0 + e];
+                    const double av = P.a[a0 + e], bv = P.b[a0 + e];     // (one round trip)
+                    const int lr = (int)(rc >> 16);
+                    const int r = lr < p ? lr : lr + nd;
+                    if (r >= r0 && r < r1) {
+                        const double v = fma(-sigma, bv, alpha * av);   // alpha A - sigma B
+                        buf[r - r0] = v;
+                        mx = fmax(mx, fabs(v));
+                    }
+                }
+                int ib = ia;                                      // child rows [ia, ib) land in [r0, r1)
+                if (jk >= 0) {
+                    int lo = ia, hi = min(mcq, ia + kAsmChunk);
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if ((int)s_pos[mo + mid] < r1) lo = mid + 1; else hi = mid;
+                    }
+                    ib = lo;
+                }
+                unsigned act = __ballot_sync(0xffffffffu, jk >= 0 && ib > ia);
+                __syncwarp();
+                // children in order; the next child's run is loaded while the current one is added
+                constexpr int UC = kAsmChunk / 32;
+                double v[UC];
+                int i0 = 0, i1 = 0, mof = 0;
+                auto fetch = [&](int q, double* w, int& a0_, int& a1_, int& mo_) {
+                    const int j = __shfl_sync(0xffffffffu, jk, q);
+                    a0_ = __shfl_sync(0xffffffffu, ia, q);
+                    a1_ = __shfl_sync(0xffffffffu, ib, q);
+                    const AsmKid& k = s_kid[q];
+                    mo_ = k.moff;
+                    const double* __restrict__ colc = k.F + (size_t)(k.ec + j) * k.ldc + k.ec;
+#pragma unroll
+                    for (int u = 0; u < UC; ++u) {
+                        const int i = a0_ + lane + 32 * u;
+                        w[u] = i < a1_ ? colc[i] : 0.0;
+                    }
+                };
+                if (act) { fetch(__ffs(act) - 1, v, i0, i1, mof); act &= act - 1; }
+                for (bool more = i1 > i0; more;) {
+                    double vn[UC];
+                    int n0 = 0, n1 = 0, nmo = 0;
+                    more = act != 0;
+                    if (more) { fetch(__ffs(act) - 1, vn, n0, n1, nmo); act &= act - 1; }
+#pragma unroll
+                    for (int u = 0; u < UC; ++u) {
+                        const int i = i0 + lane + 32 * u;
+                        if (i < i1) buf[(int)s_pos[mof + i] - r0] += v[u];
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < UC; ++u) v[u] = vn[u];
+                    i0 = n0; i1 = n1; mof = nmo;
+                }
+                ia = ib;
+                double* dst = F + (size_t)c * ld;
+#pragma unroll
+                for (int u = 0; u < kAsmChunk / 32; ++u) {
+                    const int r = r0 + lane + 32 * u;
+                    if (r < r1) dst[r] = buf[lane + 32 * u];
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        for (int j = clo + warp; j < chi; j += kAsmNW)
+            for (int i = j + lane; i < fo; i += 32) F[i + (size_t)j * ld] = 0.0;
+        __syncthreads();
+        const int e0 = clo < p ? acol[clo] : acol[p], e1 = clo < p ? acol[min(chi, p)] : acol[p];
+        for (int e = e0 + tid; e < e1; e += kAsmThreads) {
+            const uint32_t rc = P.asm_rc[a0 + e];
+            const int lr = (int)(rc >> 16), lc = (int)(rc & 0xffffu);
+            const int r = lr < p ? lr : lr + nd;
+            const double v = fma(-sigma, P.b[a0 + e], alpha * P.a[a0 + e]);
+            F[r + (size_t)lc * ld] = v;
+            mx = fmax(mx, fabs(v));
+        }
     }
-    mx = block_max<kAsmThreads>(mx, s_red);
-    if (threadIdx.x == 0 && mx > 0.0) atomic_max_pos_double(&st->smax_bits, mx);
-    // a2: extend-add, children in a fixed order
-    int off = 0;
-    for (int q = c0; q < c1; ++q) {
-        const int c = P.child_list[q];
+    mx = block_max<kAsmThreads>(mx, s_red);                     // (barrier: the gathered columns are written)
+    if (tid == 0 && mx > 0.0) atomic_max_pos_double(&st->smax_bits, mx);
+    if (gather && !s_anyd) return;
+    // RED adds, children in order: delayed columns only (gather path) or everything (plain path)
+    int doffs = 0;
+    for (int q = 0; q < nch; ++q) {
+        const int c = P.child_list[c0 + q];
         const int ndo = nd_out[c];
-        const int fc = P.forder[c] + nd_in[c];       // child order
-        const int ldc = ldpad(fc);                   // child leading dimension
+        const int dof = p + doffs;
+        doffs += ndo > 0 ? ndo : 0;
+        if (gather && ndo <= 0) continue;
+        const int fc = P.forder[c] + nd_in[c];
+        const int ldc = ldpad(fc);
         const int mc = ndo + P.ncb[c];
         const int ec = fc - mc;
         const double* __restrict__ Fc = arena + P.arena_off[c];
-        double* __restrict__ Fp = F;
-        // fast-path children keep the CB rows of their delayed columns in W21 (upper part)
         const bool wup = P.flag[(size_t)sh * P.nf + c] == FL_OK && ndo > 0;
         const int32_t* __restrict__ rm = P.rmap + P.rmap_ptr[c];
-        const int dof = p + off;
-        off += ndo > 0 ? ndo : 0;
-        const bool staged = mc <= kAsmMapMax;
-        __syncthreads();                                         // s_pos reuse
-        if (staged)
-            for (int x = threadIdx.x; x < mc; x += kAsmThreads) {
-                int v;
-                if (x < ndo) v = dof + x;
-                else { const int r = rm[x - ndo]; v = r < p ? r : r + nd; }
-                s_pos[x] = v;
-            }
-        __syncthreads();
         auto pos = [&](int x) -> int {
-            if (staged) return s_pos[x];
             if (x < ndo) return dof + x;
             const int r = rm[x - ndo];
             return r < p ? r : r + nd;
         };
-        constexpr int U = 4;                                     // rows in flight per lane
-        for (int j = warp; j < mc; j += nw) {
+        const int jend = gather ? ndo : mc;
+        __syncthreads();                                          // previous child's adds issued in order
+        for (int j = warp; j < jend; j += kAsmNW) {
             const int pj = pos(j);
-            // non-delayed child columns land in parent column pj (positions increase with the
-            // child index there); delayed columns are filtered entry by entry
             if (j >= ndo && (pj < clo || pj >= chi)) continue;
             const double* __restrict__ colc = Fc + (size_t)(ec + j) * ldc + ec;
-            for (int i0 = j; i0 < mc; i0 += 32 * U) {
-                double v[U];
-                size_t dst[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + lane + 32 * u;
-                    dst[u] = SIZE_MAX;
-                    v[u] = 0.0;
-                    if (i < mc) {
-                        const int pi = pos(i);
-                        const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
-                        if (lo >= clo && lo < chi) {
-                            dst[u] = hi + (size_t)lo * ld;
-                            v[u] = (wup && j < ndo && i >= ndo) ? Fc[(ec + j) + (size_t)(ec + i) * ldc] : colc[i];
-                        }
-                    }
-                }
-                // one writer per parent entry and child (children ordered by the barrier
-                // between them): fire-and-forget RED adds, no load latency
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (dst[u] != SIZE_MAX) atomicAdd(&Fp[dst[u]], v[u]);
+            for (int i = j + lane; i < mc; i += 32) {
+                const int pi = pos(i);
+                const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
+                if (lo < clo || lo >= chi) continue;
+                const double v = (wup && j < ndo && i >= ndo) ? Fc[(ec + j) + (size_t)(ec + i) * ldc] : colc[i];
+                atomicAdd(&F[hi + (size_t)lo * ld], v);
             }
         }
     }
 }
 
-__global__ void __launch_bounds__(kAsmThreads) k_assemble(DevPlan P, const int32_t* __restrict__ list, int S) {
-    assemble_front(P, list, S, 0);
+__global__ void __launch_bounds__(kAsmThreads, 4) k_assemble(DevPlan P, const int4* __restrict__ items) {
+    const int4 itm = items[blockIdx.x];
+    assemble_strip(P, itm.x, itm.y, itm.z, 0);
 }
 
-// restore of fronts whose fast-path pass failed: the same assembly, flagged fronts only
-__global__ void __launch_bounds__(kAsmThreads) k_reassemble(DevPlan P, const int32_t* __restrict__ list, int S) {
-    assemble_front(P, list, S, 1);
+// restore of fronts whose fast-path pass failed: the same assembly, flagged fronts only;
+// item (front, x0, S, R): strips x0, x0 + R, ... (few CTAs per front: most fronts exit at once)
+__global__ void __launch_bounds__(kAsmThreads, 4) k_reassemble(DevPlan P, const int4* __restrict__ items) {
+    const int4 itm = items[blockIdx.x];
+    for (int x = itm.y; x < itm.z; x += itm.w) {
+        assemble_strip(P, itm.x, x, itm.z, 1);
+        __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------- a3 + a4 + a5 (reference)
@@ -473,14 +616,23 @@ __global__ void k_reset_stats(ShiftStat* st, int batch) {
 
 }  // namespace
 
-void launch_assemble(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, bool only_flagged,
-                     cudaStream_t st) {
-    if (nfronts <= 0) return;
-    // CTAs per front: enough to give ~4 resident CTAs per SM on the whole level
-    int S = (int)((4 * 148 + (int64_t)nfronts * batch - 1) / ((int64_t)nfronts * batch));
-    S = std::max(1, std::min(S, 16));
-    if (only_flagged) k_reassemble<<<dim3(nfronts * S, batch), kAsmThreads, 0, st>>>(P, fronts, S);
-    else k_assemble<<<dim3(nfronts * S, batch), kAsmThreads, 0, st>>>(P, fronts, S);
+// items: (front, strip x, strips S, R) per CTA (api.cu build_lists)
+void launch_assemble(const DevPlan& P, const int4* items, int nitems, int batch, bool only_flagged, cudaStream_t st) {
+    if (nitems <= 0) return;
+    const size_t smem = sizeof(double) * kAsmNW * kAsmChunk;
+    static bool attr = false;                 // static + dynamic shared memory above 48 KB: opt in
+    if (!attr) {
+        cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_reassemble, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    if (only_flagged) k_reassemble<<<dim3(nitems, batch), kAsmThreads, smem, st>>>(P, items);
+    else k_assemble<<<dim3(nitems, batch), kAsmThreads, smem, st>>>(P, items);
+}
+
+int assembly_strips(int forder) {
+    const int64_t T = (int64_t)forder * (forder + 1) / 2;
+    return (int)std::max<int64_t>(1, (T + kAsmStripEnt - 1) / kAsmStripEnt);
 }
 
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,

@@ -56,6 +56,9 @@ constexpr int LB = 32;                          // k_l21 column block
 constexpr int LST = 3;                          // k_l21 cp.async pipeline depth
 static_assert(LT == 8 * LB, "k_l21 column-max reduction maps 8 threads to a column");
 constexpr int KC = 16;                          // K chunk of the k_l21 GEMM
+constexpr int kXMin = 64;                       // k_l21<2> (GEMM in-block solve) from this FS capacity
+constexpr int kXMaxBlocks = 256;                // ... up to this many column blocks
+constexpr int XPW = 4;                          // k_l21x_prep warps per CTA
 constexpr int APAD = LR + 4;                    // = 4 (mod 16): conflict-free f64 fragments
 constexpr int BP = KC + 4;
 
@@ -589,19 +592,27 @@ __global__ void __launch_bounds__(UT) k_fsu(DevPlan P, const int4* __restrict__ 
 // W21 = A21 P^T L11^-T for 64 CB rows of one front; column maxima of W21.
 // L11[i,t] = 0 for t >= e (delayed columns have no pivot: their W21 column
 // is the fully updated CB part of the delayed column).
+// MODE 0: in-block solve by the paired-thread triangle (below).
+// MODE 1 (SMALL): fronts with q < LB (one column block, no GEMM, compact shared memory).
+// MODE 2 (XM): the in-block solve as a second DMMA GEMM with the block's precomputed
+//   X = [L_bb^-T | L_bb^-T D^-1 M] (k_l21x_prep): [W | G] = R X with R = A21 P^T - G_prev B'_prev^T.
+template <int MODE>
 __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict__ items) {
+    constexpr bool SMALL = MODE == 1, XM = MODE == 2;
     extern __shared__ __align__(16) double l21_smem[];
+    constexpr int OFF_S = SMALL ? 0 : LST * LR * BP + LST * LB * BP;
     double (*As)[LR][BP] = reinterpret_cast<double (*)[LR][BP]>(l21_smem);                       // [LST][LR][BP] rows x t
     double (*Bs)[LB][BP] = reinterpret_cast<double (*)[LB][BP]>(l21_smem + LST * LR * BP);        // [LST][LB][BP]
-    double (*Sbase)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * LR * BP + LST * LB * BP);
+    double (*Sbase)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + OFF_S);
     static_assert(LR * (LB + 1) <= LST * LR * BP, "Sacc aliases As");
     static_assert(LB * (LB + 1) <= LST * LB * BP, "Lbb aliases Bs");
     double (*Sacc)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem);
-    double (*Lbb)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + LST * LR * BP);
+    double (*Lbb)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(l21_smem + (SMALL ? LR * (LB + 1) : LST * LR * BP));
     __shared__ int sperm[LB];
     __shared__ unsigned long long SgB[LST][KC];          // sign bits of B' = G11 S for the K chunks
     __shared__ int skind[LB];                             // pivot kind of the block columns (-1: delayed / none)
     __shared__ double sgca[LB], sgcb[LB];
+    __shared__ double cmx[4][LB];                         // XM: column maxima of |W| per 32-row slice
     const int4 it = items[blockIdx.x];
     const int s = it.x, I = it.y;
     const int sh = blockIdx.y;
@@ -622,10 +633,12 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
     const int g = lane >> 2, tg = lane & 3;
     const int wm = warp * 16;
     const int row = tid >> 1, half = tid & 1;               // triangle: two threads per CB row
-    for (int b0 = 0, nbc = 0; b0 < q; b0 += nbc) {
+    const double* Xg = XM ? P.xscr + (size_t)sh * P.xstride + P.xoff[s] : nullptr;
+    for (int b0 = 0, nbc = 0, blk = 0; b0 < q; b0 += nbc, ++blk) {
         nbc = min(LB, q - b0);
         if (nbc == LB && b0 + LB - 1 < e && A.kind[b0 + LB - 1] == PK_2X2A) nbc = LB - 1;   // keep 2x2 pairs whole
-        const int K = min(b0, e);
+        const int K = SMALL ? 0 : min(b0, e);
+        if (SMALL && b0 > 0) return;    // unreachable: the host routes only q < LB here (one block)
         if (tid < LB) {
             const int t = b0 + tid;
             sperm[tid] = tid < nbc ? A.perm[t] : 0;
@@ -648,7 +661,7 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
         for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
-        if (K > 0) {
+        if (!SMALL && K > 0) {
             auto load = [&](int buf, int t0) {
                 for (int x = tid; x < (KC / 2) * LR; x += LT) {   // G rows: 16-byte pairs (even ld, t0 % 16 == 0)
                     const int ii = x / (KC / 2), tt = 2 * (x - ii * (KC / 2));
@@ -700,12 +713,91 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
             cp_async_wait<0>();
             __syncthreads();
         }
+        if (XM) {
+            constexpr int XP = LB + 4;                          // = 4 (mod 16): conflict-free f64 fragments
+            static_assert(LR * XP + 2 * LB * XP <= LST * LR * BP, "R and X alias As");
+            double (*Rs)[XP] = reinterpret_cast<double (*)[XP]>(l21_smem);
+            double (*Xs)[XP] = reinterpret_cast<double (*)[XP]>(l21_smem + LR * XP);
+            const double* xb = Xg + (size_t)blk * (2 * LB * LB);
+            for (int x = tid; x < 2 * LB * (LB / 2); x += LT) {    // X block [n][k], 64 x 32
+                const int n = x / (LB / 2), k2 = 2 * (x - n * (LB / 2));
+                cp_async16(&Xs[n][k2], xb + n * LB + k2, 16);
+            }
+            cp_async_commit();
 #pragma unroll
-        for (int mb = 0; mb < 2; ++mb)
+            for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
-            for (int nb = 0; nb < 4; ++nb)
+                for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-                for (int h = 0; h < 2; ++h) Sacc[wm + 8 * mb + g][8 * nb + 2 * tg + h] = acc[mb][nb][h];
+                    for (int h = 0; h < 2; ++h) {
+                        const int rr = wm + 8 * mb + g, cc = 8 * nb + 2 * tg + h;
+                        Rs[rr][cc] = Sbase[rr][cc] - acc[mb][nb][h];
+                    }
+            cp_async_wait<0>();
+            __syncthreads();
+            const int wm2 = (warp >> 1) * 32, wn2 = (warp & 1) * 32;     // 4 x 2 warps of 32 x 32
+            double acc2[4][4][2];
+#pragma unroll
+            for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) acc2[mb][nb][0] = acc2[mb][nb][1] = 0.0;
+#pragma unroll
+            for (int k4 = 0; k4 < LB; k4 += 4) {
+                double a[4], b[4];
+#pragma unroll
+                for (int mb = 0; mb < 4; ++mb) a[mb] = Rs[wm2 + 8 * mb + g][k4 + tg];
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) b[nb] = Xs[wn2 + 8 * nb + g][k4 + tg];
+#pragma unroll
+                for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) dmma(acc2[mb][nb], a[mb], b[nb]);
+            }
+            if (wn2 == 0) {                                     // W: column maxima (threshold tests, k_check)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        double m = 0.0;
+#pragma unroll
+                        for (int mb = 0; mb < 4; ++mb) m = fmax(m, fabs(acc2[mb][nb][h]));
+                        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 4));
+                        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 8));
+                        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 16));
+                        if (g == 0) cmx[wm2 / 32][8 * nb + 2 * tg + h] = m;
+                    }
+            } else {                                            // G rows to the upper part
+#pragma unroll
+                for (int mb = 0; mb < 4; ++mb) {
+                    const int i = r0 + wm2 + 8 * mb + g;
+                    if (i >= f) continue;
+                    double* __restrict__ Gi = F + (size_t)i * ld + b0;
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int t = 8 * nb + 2 * tg + h;
+                            if (t < nbc) Gi[t] = acc2[mb][nb][h];
+                        }
+                }
+            }
+            __syncthreads();
+            if (tid < LB) {
+                const double m = fmax(fmax(cmx[0][tid], cmx[1][tid]), fmax(cmx[2][tid], cmx[3][tid]));
+                if (tid < nbc && b0 + tid < e && m > 0.0)
+                    atomicMax(&A.cm[b0 + tid], (unsigned long long)__double_as_longlong(m));
+            }
+            __syncthreads();                                    // Rs / Xs (As) and Sbase free for the next block
+            continue;
+        }
+        if (!SMALL) {
+#pragma unroll
+            for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) Sacc[wm + 8 * mb + g][8 * nb + 2 * tg + h] = acc[mb][nb][h];
+        }
         // diagonal block of B' = L11 D M^-T = G11 S (strict lower, columns < e only)
         for (int x = tid; x < LB * LB; x += LT) {           // consecutive threads walk a column (coalesced)
             const int b = x / LB, a = x - b * LB;
@@ -723,6 +815,7 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
             double vprev = 0.0;
 #pragma unroll
             for (int t = 0; t < LB; ++t) {
+                if (t >= nbc) break;                         // (uniform)
                 double p0 = 0.0, p1 = 0.0;
 #pragma unroll
                 for (int u = 0; 2 * u + half < t && u < LB / 2; u += 2) {
@@ -731,7 +824,7 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
                 }
                 const double part = p0 + p1;
                 const double tot = part + __shfl_xor_sync(0xffffffffu, part, 1);
-                double v = Sbase[row][t] - Sacc[row][t] - tot;
+                double v = SMALL ? Sbase[row][t] - tot : Sbase[row][t] - Sacc[row][t] - tot;
                 v = (t < nbc && valid) ? v : 0.0;
                 const int kd = skind[t];
                 const bool own = (t & 1) == half;
@@ -767,6 +860,95 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
                 atomicMax(&A.cm[b0 + t], (unsigned long long)__double_as_longlong(m));
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ k_l21x_prep
+// Per front and column block [b0, b0 + nbc) of k_l21 (the same block rule): the
+// unit lower block L_bb of L11 (from the stored G11 = L11 M: L = G11 S (D M^-T)^-1,
+// as in k_store), its inverse by forward substitution (one lane per column), and
+//   X[n][k] = L_bb^-1[n][k]                               n < 32   (W = R L_bb^-T)
+//   X[32 + t][k] = L_bb^-1[t][k] gca[t] + L_bb^-1[t'][k] gcb[t]     (G = W D^-1 M,
+//                  t' the 2x2 partner; delayed columns: G = W)
+// stored [n][k] (k contiguous) in the level's X scratch for k_l21<2>.
+__global__ void __launch_bounds__(XPW * 32) k_l21x_prep(DevPlan P, const int32_t* __restrict__ fronts) {
+    extern __shared__ double xp_smem[];                   // [XPW][LB][LB + 1]
+    __shared__ int sb0[kXMaxBlocks], snb[kXMaxBlocks];
+    __shared__ int s_nblk;
+    const int s = fronts[blockIdx.x];
+    const int sh = blockIdx.y;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    if (nd < 0) return;
+    if (P.flag[(size_t)sh * P.nf + s] != FL_ACTIVE) return;
+    const int ndo = P.nd_out[(size_t)sh * P.nf + s];
+    if (ndo < 0) return;
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
+    const int e = q - ndo;
+    const double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
+    double* X = P.xscr + (size_t)sh * P.xstride + P.xoff[s];
+    if (threadIdx.x == 0) {
+        int nb = 0;
+        for (int b0 = 0, nbc = 0; b0 < q && nb < kXMaxBlocks; b0 += nbc) {
+            nbc = min(LB, q - b0);
+            if (nbc == LB && b0 + LB - 1 < e && A.kind[b0 + LB - 1] == PK_2X2A) nbc = LB - 1;   // as k_l21
+            sb0[nb] = b0; snb[nb] = nbc; ++nb;
+        }
+        s_nblk = nb;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double (*Lw)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(xp_smem + (size_t)warp * LB * (LB + 1));
+    // L[i][t] for a pivot column t < e (rows i > t of the block): from B' = G11 S
+    auto lval = [&](int i, int t) -> double {
+        const int kd = A.kind[t];
+        double v = F[i + (size_t)t * ld] * A.sgn[t] * A.gca[t];
+        if (kd == PK_2X2A) v = (i == t + 1) ? 0.0 : v + F[i + (size_t)(t + 1) * ld] * A.sgn[t + 1] * A.gcb[t + 1];
+        else if (kd == PK_2X2B) v += F[i + (size_t)(t - 1) * ld] * A.sgn[t - 1] * A.gcb[t - 1];
+        else if (kd == PK_ZERO) v = 0.0;
+        return v;
+    };
+    for (int bk = warp; bk < s_nblk; bk += XPW) {
+        const int b0 = sb0[bk], nbc = snb[bk];
+        for (int x = lane; x < LB * LB; x += 32) {         // strict lower L_bb (zero elsewhere)
+            const int b = x / LB, a = x - b * LB;           // column b, row a (lanes walk a column)
+            Lw[a][b] = (a < nbc && b < a && b0 + b < e) ? lval(b0 + a, b0 + b) : 0.0;
+        }
+        __syncwarp();
+        // lane j: column j of L_bb^-1 (unit lower), kept transposed in the upper part: Y[t][j] -> Lw[j][t]
+        {
+            const int j = lane;
+            for (int t = j + 1; t < nbc; ++t) {
+                double acc = Lw[t][j];                      // Y[j][j] = 1
+                for (int u = j + 1; u < t; ++u) acc = fma(Lw[t][u], Lw[j][u], acc);
+                Lw[j][t] = -acc;
+            }
+        }
+        __syncwarp();
+        auto yinv = [&](int n, int k) -> double {           // L_bb^-1[n][k]
+            if (n >= nbc || k >= nbc) return 0.0;
+            return n == k ? 1.0 : (n > k ? Lw[k][n] : 0.0);
+        };
+        double* xb = X + (size_t)bk * (2 * LB * LB);
+        for (int n = 0; n < 2 * LB; ++n) {
+            const int k = lane;
+            double v;
+            if (n < LB) v = yinv(n, k);
+            else {
+                const int t = n - LB;
+                if (t >= nbc) v = 0.0;
+                else if (b0 + t >= e) v = yinv(t, k);       // delayed column: G = W
+                else {
+                    const int kd = A.kind[b0 + t];
+                    v = yinv(t, k) * A.gca[b0 + t];
+                    if (kd == PK_2X2A) v += yinv(t + 1, k) * A.gcb[b0 + t];
+                    else if (kd == PK_2X2B) v += yinv(t - 1, k) * A.gcb[b0 + t];
+                }
+            }
+            xb[n * LB + k] = v;
+        }
+        __syncwarp();
     }
 }
 
@@ -948,12 +1130,36 @@ void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cuda
     k_fsu<<<dim3(nitems, batch), UT, 0, st>>>(P, items);
 }
 
-void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
+void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, int mode, cudaStream_t st) {
     if (nitems <= 0) return;
     const size_t smem = sizeof(double) * (LST * LR * BP + LST * LB * BP + LR * (LB + 1));
+    const size_t smem_s = sizeof(double) * (LR * (LB + 1) + LB * (LB + 1));
     static bool attr = false;
-    if (!attr) { cudaFuncSetAttribute(k_l21, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
-    k_l21<<<dim3(nitems, batch), LT, smem, st>>>(P, items);
+    if (!attr) {
+        cudaFuncSetAttribute(k_l21<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_l21<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
+        cudaFuncSetAttribute(k_l21<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    if (mode == 1) k_l21<1><<<dim3(nitems, batch), LT, smem_s, st>>>(P, items);
+    else if (mode == 2) k_l21<2><<<dim3(nitems, batch), LT, smem, st>>>(P, items);
+    else k_l21<0><<<dim3(nitems, batch), LT, smem, st>>>(P, items);
+}
+
+int l21_mode(int qcap) {
+    if (qcap < LB) return 1;
+    if (qcap >= kXMin && qcap <= (LB - 1) * kXMaxBlocks) return 2;
+    return 0;
+}
+
+int64_t l21_x_doubles(int qcap) { return (int64_t)2 * LB * LB * ((qcap + LB - 2) / (LB - 1)); }
+
+void launch_l21x_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    const size_t smem = sizeof(double) * XPW * LB * (LB + 1);
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(k_l21x_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+    k_l21x_prep<<<dim3(nfronts, batch), XPW * 32, smem, st>>>(P, fronts);
 }
 
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
