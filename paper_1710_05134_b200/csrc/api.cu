@@ -69,6 +69,8 @@ struct kep_ctx {
     double* d_xscr = nullptr;
     int64_t xstride = 0;
     std::vector<int64_t> lsitem_off, lsitem_cnt, lxitem_off, lxitem_cnt, xfront_off, xfront_cnt;
+    struct FsGroup { int64_t foff, fcnt, uoff, ucnt; int qmax; };
+    std::vector<std::vector<FsGroup>> fs_groups;   // per level: fast fronts by FS capacity (k_fsp/k_fsu passes)
     int4* d_aitems = nullptr;                   // k_assemble strips (front, x, S, 0): all fronts, then fast fronts
     std::vector<int64_t> aitem_off, aitem_cnt, raitem_off, raitem_cnt;
     std::vector<int64_t> fast_off, fast_cnt, ref_off, ref_cnt, item_off, item_cnt, litem_off, litem_cnt;
@@ -228,6 +230,7 @@ kep_status build_lists(kep_ctx* c) {
     c->ref_off.assign(nl, 0); c->ref_cnt.assign(nl, 0);
     c->item_off.assign(nl, 0); c->item_cnt.assign(nl, 0);
     c->level_qmax.assign(nl, 0);
+    c->fs_groups.clear();
     for (int L = 0; L < nl; ++L) {
         c->fast_off[L] = (int64_t)fast.size();
         c->ref_off[L] = (int64_t)ref.size();
@@ -247,34 +250,76 @@ kep_status build_lists(kep_ctx* c) {
             if (use_fast && kep::front_nb_for(S.capacity[S.level_fronts[k]] - S.ncb[S.level_fronts[k]]) > 0)
                 strips(S.level_fronts[k], 8);
         c->raitem_cnt[L] = (int64_t)aitems.size() - c->raitem_off[L];
+        // tile lists in the level's front order
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
             const int s = S.level_fronts[k];
             const int qcap = S.capacity[s] - S.ncb[s];            // p + slack
-            if (use_fast && kep::front_nb_for(qcap) > 0) {
-                fast.push_back(s);
-                c->level_qmax[L] = std::max(c->level_qmax[L], qcap);
-                const int lmode = kep::l21_mode(qcap);
-                auto& li = lmode == 1 ? lsitems : (lmode == 2 ? lxitems : litems);
-                if (lmode == 2) {
-                    xfronts.push_back(s);
-                    xoff[s] = xacc;
-                    xacc += kep::l21_x_doubles(qcap);
-                }
-                for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) li.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
-                for (int I = 0; I < (qcap + 63) / 64; ++I)
-                    for (int J = 0; J <= I; ++J) uitems.push_back(make_int4(s, I, J, 0));
-                if (kep::schur_small_ok(S.ncb[s], qcap)) {
-                    small.push_back(s);                                  // whole CB in one CTA
-                } else {
-                    const int nt = (S.ncb[s] + 63) / 64;
-                    for (int I = 0; I < nt; ++I)
-                        for (int J = 0; J <= I; ++J) items.push_back(make_int4(s, I, J, 0));
-                }
-            } else {
+            if (!(use_fast && kep::front_nb_for(qcap) > 0)) {
                 ref.push_back(s);
+                continue;
+            }
+            c->level_qmax[L] = std::max(c->level_qmax[L], qcap);
+            const int lmode = kep::l21_mode(qcap);
+            auto& li = lmode == 1 ? lsitems : (lmode == 2 ? lxitems : litems);
+            if (lmode == 2) {
+                xfronts.push_back(s);
+                xoff[s] = xacc;
+                xacc += kep::l21_x_doubles(qcap);
+            }
+            for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) li.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
+            if (kep::schur_small_ok(S.ncb[s], qcap)) {
+                small.push_back(s);                                  // whole CB in one CTA
+            } else {
+                const int nt = (S.ncb[s] + 63) / 64;
+                for (int I = 0; I < nt; ++I)
+                    for (int J = 0; J <= I; ++J) items.push_back(make_int4(s, I, J, 0));
             }
         }
+        // fast fronts (and their k_fsu tiles) in increasing FS capacity: the k_fsp/k_fsu passes
+        // run per size group
+        std::vector<int> lf(S.level_fronts.begin() + S.level_ptr[L], S.level_fronts.begin() + S.level_ptr[L + 1]);
+        std::stable_sort(lf.begin(), lf.end(), [&](int a, int b) {
+            return S.capacity[a] - S.ncb[a] < S.capacity[b] - S.ncb[b];
+        });
+        std::vector<int64_t> fu;                                  // uitems offset of each fast front
+        for (int s : lf) {
+            const int qcap = S.capacity[s] - S.ncb[s];
+            if (!(use_fast && kep::front_nb_for(qcap) > 0)) continue;
+            fast.push_back(s);
+            fu.push_back((int64_t)uitems.size());
+            for (int I = 0; I < (qcap + 63) / 64; ++I)
+                for (int J = 0; J <= I; ++J) uitems.push_back(make_int4(s, I, J, 0));
+        }
         c->fast_cnt[L] = (int64_t)fast.size() - c->fast_off[L];
+        {   // size groups: at most three contiguous ranges of the sorted fast fronts, chosen by fs_cost
+            const int64_t n = c->fast_cnt[L], f0 = c->fast_off[L];
+            const int64_t mb = std::max(1, std::min(c->opts.max_batch, 8));
+            fu.push_back((int64_t)uitems.size());
+            auto qc = [&](int64_t x) { return S.capacity[fast[f0 + x]] - S.ncb[fast[f0 + x]]; };
+            auto cost = [&](int64_t a, int64_t b) { return b > a ? kep::fs_cost(qc(b - 1), (b - a) * mb) : 0.0; };
+            std::vector<int64_t> cuts;                             // candidate split points (qcap changes)
+            for (int64_t x = 1; x < n; ++x)
+                if (qc(x) != qc(x - 1)) cuts.push_back(x);
+            double best = cost(0, n);
+            int64_t b1 = n, b2 = n;
+            for (size_t i = 0; i < cuts.size(); ++i) {
+                const int64_t x = cuts[i];
+                const double c2 = cost(0, x) + cost(x, n);
+                if (c2 < best) { best = c2; b1 = x; b2 = n; }
+                for (size_t j = i + 1; j < cuts.size(); ++j) {
+                    const int64_t y = cuts[j];
+                    const double c3 = cost(0, x) + cost(x, y) + cost(y, n);
+                    if (c3 < best) { best = c3; b1 = x; b2 = y; }
+                }
+            }
+            std::vector<kep_ctx::FsGroup> gs;
+            const int64_t bnd[4] = {0, b1, b2, n};
+            for (int k2 = 0; k2 < 3; ++k2)
+                if (bnd[k2 + 1] > bnd[k2])
+                    gs.push_back({f0 + bnd[k2], bnd[k2 + 1] - bnd[k2], fu[bnd[k2]], fu[bnd[k2 + 1]] - fu[bnd[k2]],
+                                  (int)qc(bnd[k2 + 1] - 1)});
+            c->fs_groups.push_back(gs);
+        }
         c->ref_cnt[L] = (int64_t)ref.size() - c->ref_off[L];
         c->item_cnt[L] = (int64_t)items.size() - c->item_off[L];
         c->litem_cnt[L] = (int64_t)litems.size() - c->litem_off[L];
@@ -564,29 +609,36 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 const int nfl2 = (int)c->fast_cnt[L];
                 // pass 0, then kReruns passes over the fronts whose full-column test failed
                 // (each with one more forced delay), then the unblocked kernel for the rest
-                int iters = kep::fs_iters(c->level_qmax[L], (int64_t)nfl2 * m);
+                const auto& groups = c->fs_groups[L];
+                int pend_q = INT_MAX;                   // rerun passes: largest flagged FS block
                 for (int pass = 0; pass <= kReruns; ++pass) {
                     if (pass > 0) {                     // any front flagged for a rerun at this level?
                         int32_t pend[2] = {0, 0};
                         KEP_CUDA(c, cudaMemcpyAsync(pend, c->d_pending, sizeof(pend), cudaMemcpyDeviceToHost, c->stream));
                         KEP_CUDA(c, cudaStreamSynchronize(c->stream));
                         if (pend[0] == 0) break;
-                        // the rerun pass only needs the pivot blocks of the largest flagged FS block
-                        // (at the level's block width)
-                        const int nbl = kep::front_nb_for(c->level_qmax[L], (int64_t)nfl2 * m);
-                        iters = std::min(iters, (pend[1] + nbl - 2) / (nbl - 1) + 1);
+                        pend_q = pend[1];
                     }
                     KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
-                    for (int itn = 0; itn < iters; ++itn) {
-                        mark(KEP_K_PANEL, true);
-                        kep::launch_fsp(P, fl, nfl2, m, c->level_qmax[L], itn == 0 ? (pass == 0 ? 0 : 1) : 2, c->stream);
-                        mark(KEP_K_PANEL, false);
-                        c->prof.launches[KEP_K_PANEL]++;
-                        if (c->uitem_cnt[L]) {
-                            mark(KEP_K_FSU, true);
-                            kep::launch_fsu(P, c->d_uitems + c->uitem_off[L], (int)c->uitem_cnt[L], m, c->stream);
-                            mark(KEP_K_FSU, false);
-                            c->prof.launches[KEP_K_FSU]++;
+                    for (const auto& gr : groups) {     // size groups of the level's fast fronts
+                        const int64_t nbk = gr.fcnt * m;
+                        int iters = kep::fs_iters(gr.qmax, nbk);
+                        if (pass > 0) {                 // only the pivot blocks of the largest flagged FS block
+                            const int nbl = kep::front_nb_for(gr.qmax, nbk);
+                            iters = std::min(iters, (std::min(pend_q, gr.qmax) + nbl - 2) / (nbl - 1) + 1);
+                        }
+                        for (int itn = 0; itn < iters; ++itn) {
+                            mark(KEP_K_PANEL, true);
+                            kep::launch_fsp(P, c->d_lists + gr.foff, (int)gr.fcnt, m, gr.qmax,
+                                            itn == 0 ? (pass == 0 ? 0 : 1) : 2, c->stream);
+                            mark(KEP_K_PANEL, false);
+                            c->prof.launches[KEP_K_PANEL]++;
+                            if (gr.ucnt) {
+                                mark(KEP_K_FSU, true);
+                                kep::launch_fsu(P, c->d_uitems + gr.uoff, (int)gr.ucnt, m, c->stream);
+                                mark(KEP_K_FSU, false);
+                                c->prof.launches[KEP_K_FSU]++;
+                            }
                         }
                     }
                     if (c->litem_cnt[L] || c->lsitem_cnt[L] || c->lxitem_cnt[L]) {

@@ -144,6 +144,7 @@ int assembly_strips(int forder);     // CTAs (column strips) per front of the gi
 void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int qmax, int mode, cudaStream_t st);
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
 int fs_iters(int qmax, int64_t nblocks);   // k_fsp launches that finish every front of a level
+double fs_cost(int qmax, int64_t nblocks);  // planning model of a group's k_fsp/k_fsu passes
 bool fs_uses_gls(int qmax);                 // the level's block columns live in global scratch
 int fs_rows_pad(int qmax);
 size_t fs_gls_doubles(int nb, int RS);

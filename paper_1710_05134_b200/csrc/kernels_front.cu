@@ -1125,6 +1125,21 @@ void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch,
 #undef KEP_FSP
 }
 
+// Model of the k_fsp + k_fsu passes of one group of fronts (host planning of the
+// per-level size buckets): launches x waves x block columns, + a launch overhead.
+double fs_cost(int qmax, int64_t nblocks) {
+    const int nb = front_nb_for(qmax, nblocks);
+    if (nb <= 0) return 0.0;
+    const int RS = fs_rows_pad(qmax);
+    const bool gls = fs_uses_gls(qmax);
+    const double smem = (double)fs_smem_bytes(nb, RS, gls) + 2048.0;
+    const int th = gls ? 256 : (qmax <= 40 ? 32 : (qmax <= 192 ? 128 : 256));
+    const int cps = std::max(1, std::min((int)(233472.0 / smem), 2048 / th));
+    const double waves = std::ceil((double)nblocks / (148.0 * cps));
+    const double iters = (double)fs_iters(qmax, nblocks);
+    return iters * (waves * nb + 12.0);
+}
+
 void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
     if (nitems <= 0) return;
     k_fsu<<<dim3(nitems, batch), UT, 0, st>>>(P, items);

@@ -3,9 +3,12 @@ configs, for the GPU parity tests at BASELINE sizes.
 
 Calls only ``oracle/`` (O-sparse multifrontal) and the seeded generator
 ``kepgen``.  Each shift is certified by the oracle itself: nu(sigma - d) ==
-nu(sigma) == nu(sigma + d) with d = 1e-6 * max(|lo|, |hi|) (R5).
+nu(sigma) == nu(sigma + d), i.e. no eigenvalue within d of sigma, with
+d = 1e-3 (hi - lo) / n (a thousandth of the mean eigenvalue spacing, still many
+orders above the backward error of the factorisation; R5).
+``--reuse FILE`` takes nu(sigma) from an earlier run at the same shifts.
 
-    python scripts/make_goldens.py 2 [4] [--shifts 8] [--procs 8]
+    python scripts/make_goldens.py 2 [4] [--shifts 8] [--procs 8] [--reuse old.json]
 """
 import argparse
 import json
@@ -43,6 +46,7 @@ def main():
     ap.add_argument("configs", type=int, nargs="+")
     ap.add_argument("--shifts", type=int, default=8)
     ap.add_argument("--procs", type=int, default=8)
+    ap.add_argument("--reuse", default=None)
     a = ap.parse_args()
     import numpy as np
     import kepgen
@@ -50,15 +54,23 @@ def main():
         p = kepgen.config(cfg)
         lo, hi = kepgen.spectral_bounds(p)
         sig = kepgen.uniform_shifts(lo, hi, a.shifts)
-        d = 1e-6 * max(abs(lo), abs(hi))
+        d = 1e-3 * (hi - lo) / p.n
+        old = {}
+        if a.reuse:
+            for x in json.load(open(a.reuse))["shifts"]:
+                old[x["sigma"]] = (x["sigma"], x["nu"], x["oracle_delayed"], False, x["oracle_seconds"])
         todo = []
         for s in sig:
-            todo += [s - d, s, s + d]
+            todo += [s - d] + ([] if float(s) in old else [s]) + [s + d]
         with get_context("fork").Pool(a.procs, initializer=_init, initargs=(cfg,)) as pool:
             res = pool.map(_nu, todo)
         out = []
-        for i, s in enumerate(sig):
-            (_, nm, _, sm, _), (_, n0, dl, s0, t0), (_, npl, _, sp, _) = res[3 * i:3 * i + 3]
+        it = iter(res)
+        for s in sig:
+            r_m = next(it)
+            r_0 = old[float(s)] if float(s) in old else next(it)
+            r_p = next(it)
+            (_, nm, _, sm, _), (_, n0, dl, s0, t0), (_, npl, _, sp, _) = r_m, r_0, r_p
             out.append(dict(sigma=float(s), nu=n0, certified=bool(nm == n0 == npl and not (sm or s0 or sp)),
                             oracle_delayed=dl, oracle_seconds=t0))
         doc = {"_source": f"scripts/make_goldens.py: oracle.sparse_mf (O-sparse) on kepgen.config({cfg}) "
