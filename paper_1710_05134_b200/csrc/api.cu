@@ -204,6 +204,15 @@ kep_status alloc_batch(kep_ctx* c) {
 // tiles) and fronts for the reference kernel; build the Schur work items.
 kep_status build_lists(kep_ctx* c) {
     const Symbolic& S = c->sym;
+    // fast (blocked) path, or the unblocked kernel (variant 1, and tiny fronts whose whole
+    // factorisation fits one CTA's worth of work)
+    auto is_fast = [&](int s) {
+        const int qcap = S.capacity[s] - S.ncb[s];
+        if (c->opts.kernel_variant != 0 || kep::front_nb_for(qcap) <= 0) return false;
+        const char* e = getenv("KEP_TINY_REF");
+        const int tiny = e ? atoi(e) : 0;
+        return !(qcap <= tiny && S.ncb[s] <= 4 * tiny);
+    };
     const int nl = (int)S.level_ptr.size() - 1;
     const bool use_fast = c->opts.kernel_variant == 0;
     std::vector<int32_t> fast, ref;
@@ -247,14 +256,14 @@ kep_status build_lists(kep_ctx* c) {
         c->aitem_cnt[L] = (int64_t)aitems.size() - c->aitem_off[L];
         c->raitem_off[L] = (int64_t)aitems.size();
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k)
-            if (use_fast && kep::front_nb_for(S.capacity[S.level_fronts[k]] - S.ncb[S.level_fronts[k]]) > 0)
+            if (is_fast(S.level_fronts[k]))
                 strips(S.level_fronts[k], 8);
         c->raitem_cnt[L] = (int64_t)aitems.size() - c->raitem_off[L];
         // tile lists in the level's front order
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
             const int s = S.level_fronts[k];
             const int qcap = S.capacity[s] - S.ncb[s];            // p + slack
-            if (!(use_fast && kep::front_nb_for(qcap) > 0)) {
+            if (!is_fast(s)) {
                 ref.push_back(s);
                 continue;
             }
@@ -284,7 +293,7 @@ kep_status build_lists(kep_ctx* c) {
         std::vector<int64_t> fu;                                  // uitems offset of each fast front
         for (int s : lf) {
             const int qcap = S.capacity[s] - S.ncb[s];
-            if (!(use_fast && kep::front_nb_for(qcap) > 0)) continue;
+            if (!is_fast(s)) continue;
             fast.push_back(s);
             fu.push_back((int64_t)uitems.size());
             for (int I = 0; I < (qcap + 63) / 64; ++I)

@@ -1084,9 +1084,9 @@ int front_nb_for(int qmax, int64_t nblocks) {
     const int RS = fs_rows_pad(qmax);
     const size_t lim = kFsSmemLimit;
     if (fs_uses_gls(qmax)) return 16;                  // block columns in global scratch
-    // NB = 32 halves the k_fsu passes but its Ls block (q x 32) leaves one CTA per SM for q > 384:
-    // worth it only when the level is too small to fill the GPU anyway
-    const int q32 = nblocks < 4 * 148 ? 640 : 384;
+    // NB = 32 halves the k_fsu passes but its Ls block (q x 32) halves the CTAs per SM: on full
+    // levels only up to q = 256 (measured at c4: 256 > 384 > 512 > 640)
+    const int q32 = nblocks < 4 * 148 ? 640 : 256;
     if (fs_smem_bytes(32, RS, false) <= lim && qmax <= q32) return 32;
     if (fs_smem_bytes(16, RS, false) <= lim) return 16;
     if (fs_smem_bytes(8, RS, false) <= lim) return 8;
