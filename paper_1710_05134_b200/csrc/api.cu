@@ -48,6 +48,7 @@ struct kep_ctx {
     int64_t *d_arena_off = nullptr, *d_asm_ptr = nullptr, *d_asm_src = nullptr, *d_rmap_ptr = nullptr;
     uint32_t* d_asm_rc = nullptr;
     int32_t* d_asm_col = nullptr;
+    double* d_stage = nullptr;                  // kep_set_values: device copy of the host values (2 nnz)
     int32_t* d_rmap = nullptr;
     double *d_a = nullptr, *d_b = nullptr;
     // batch state
@@ -831,18 +832,18 @@ kep_status kep_set_values(kep_ctx* c, const double* a, const double* b) {
     if (!c->have_device) return fail(c, KEP_ENODEVICE, "no CUDA device");
     KEP_CUDA(c, cudaSetDevice(c->device));
     const size_t bytes = (size_t)c->sym.nnz * sizeof(double);
-    double *ta = nullptr, *tb = nullptr;
-    KEP_CUDA(c, cudaMalloc(&ta, std::max<size_t>(bytes, 8)));
-    cudaError_t e = cudaMalloc(&tb, std::max<size_t>(bytes, 8));
-    if (e != cudaSuccess) { cudaFree(ta); return fail(c, KEP_ENOMEM, "cudaMalloc failed"); }
-    e = cudaMemcpyAsync(ta, a, bytes, cudaMemcpyHostToDevice, c->stream);
+    if (!c->d_stage) {                 // staging for the host values, kept for the next call
+        cudaError_t e = cudaMalloc(&c->d_stage, 2 * std::max<size_t>(bytes, 8));
+        if (e != cudaSuccess) { c->d_stage = nullptr; return fail(c, KEP_ENOMEM, "cudaMalloc failed"); }
+    }
+    double* ta = c->d_stage;
+    double* tb = c->d_stage + std::max<size_t>(c->sym.nnz, 1);
+    cudaError_t e = cudaMemcpyAsync(ta, a, bytes, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(tb, b, bytes, cudaMemcpyHostToDevice, c->stream);
     kep_status st = KEP_OK;
     if (e != cudaSuccess) st = fail(c, KEP_ECUDA, cudaGetErrorString(e));
     else st = kep_set_values_dev(c, ta, tb);
-    cudaStreamSynchronize(c->stream);
-    cudaFree(ta);
-    cudaFree(tb);
+    cudaStreamSynchronize(c->stream);    // the caller may reuse its host buffers on return
     return st;
 }
 
@@ -1463,7 +1464,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_level_fronts, c->d_arena_off, c->d_asm_ptr, c->d_asm_src, c->d_rmap_ptr,
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
-                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
+                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
                         c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
