@@ -50,7 +50,8 @@ def build(verbose: bool = False) -> str:
             _run(["g++", "-O3", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-g",
                   "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj], log)
             objs.append(obj)
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, METIS, "-Xlinker", "--exclude-libs,ALL", "-lm"], log)
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, METIS, "-Xlinker", "--exclude-libs,ALL", "-Xlinker", "-z,defs",
+              "-lm"], log)
     if verbose:
         print(open(logpath).read())
     return LIB

@@ -49,6 +49,10 @@ struct kep_ctx {
     uint32_t* d_asm_rc = nullptr;
     int32_t* d_asm_col = nullptr;
     double* d_stage = nullptr;                  // kep_set_values: device copy of the host values (2 nnz)
+    // rerun passes: per fast front list descriptors and the compact lists (k_rerun_lists)
+    int4 *d_rr_d1 = nullptr, *d_rr_d2 = nullptr;
+    int32_t *d_rr_fr = nullptr, *d_rr_x = nullptr, *d_rr_cnt = nullptr;
+    int4 *d_rr_l[3] = {nullptr, nullptr, nullptr}, *d_rr_u = nullptr, *d_rr_a = nullptr;
     int32_t* d_rmap = nullptr;
     double *d_a = nullptr, *d_b = nullptr;
     // batch state
@@ -221,6 +225,8 @@ kep_status build_lists(kep_ctx* c) {
     std::vector<int32_t> xfronts;
     std::vector<int64_t> xoff(S.nf > 0 ? S.nf : 1, 0);
     int64_t xmax = 0;
+    std::vector<int4> rd1(S.nf > 0 ? S.nf : 1, make_int4(0, 0, 0, 0)), rd2(S.nf > 0 ? S.nf : 1, make_int4(0, 0, 0, 0));
+    int64_t mx_f = 1, mx_l[3] = {1, 1, 1}, mx_u = 1, mx_a = 1;
     std::vector<int32_t> small;
     c->litem_off.assign(nl, 0); c->litem_cnt.assign(nl, 0);
     c->lsitem_off.assign(nl, 0); c->lsitem_cnt.assign(nl, 0);
@@ -257,8 +263,12 @@ kep_status build_lists(kep_ctx* c) {
         c->aitem_cnt[L] = (int64_t)aitems.size() - c->aitem_off[L];
         c->raitem_off[L] = (int64_t)aitems.size();
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k)
-            if (is_fast(S.level_fronts[k]))
-                strips(S.level_fronts[k], 8);
+            if (is_fast(S.level_fronts[k])) {
+                const int s = S.level_fronts[k];
+                rd2[s].y = (int)aitems.size();
+                strips(s, 8);
+                rd2[s].z = (int)aitems.size() - rd2[s].y;
+            }
         c->raitem_cnt[L] = (int64_t)aitems.size() - c->raitem_off[L];
         // tile lists in the level's front order
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
@@ -276,7 +286,10 @@ kep_status build_lists(kep_ctx* c) {
                 xoff[s] = xacc;
                 xacc += kep::l21_x_doubles(qcap);
             }
+            rd1[s].x = lmode;
+            rd1[s].y = (int)li.size();
             for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) li.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
+            rd1[s].z = (int)li.size() - rd1[s].y;
             if (kep::schur_small_ok(S.ncb[s], qcap)) {
                 small.push_back(s);                                  // whole CB in one CTA
             } else {
@@ -297,8 +310,10 @@ kep_status build_lists(kep_ctx* c) {
             if (!is_fast(s)) continue;
             fast.push_back(s);
             fu.push_back((int64_t)uitems.size());
+            rd1[s].w = (int)uitems.size();
             for (int I = 0; I < (qcap + 63) / 64; ++I)
                 for (int J = 0; J <= I; ++J) uitems.push_back(make_int4(s, I, J, 0));
+            rd2[s].x = (int)uitems.size() - rd1[s].w;
         }
         c->fast_cnt[L] = (int64_t)fast.size() - c->fast_off[L];
         {   // size groups: at most three contiguous ranges of the sorted fast fronts, chosen by fs_cost
@@ -337,7 +352,13 @@ kep_status build_lists(kep_ctx* c) {
         c->lxitem_cnt[L] = (int64_t)lxitems.size() - c->lxitem_off[L];
         c->xfront_cnt[L] = (int64_t)xfronts.size() - c->xfront_off[L];
         xmax = std::max(xmax, xacc);
+        mx_f = std::max(mx_f, c->fast_cnt[L]);
+        mx_l[0] = std::max(mx_l[0], c->litem_cnt[L]);
+        mx_l[1] = std::max(mx_l[1], c->lsitem_cnt[L]);
+        mx_l[2] = std::max(mx_l[2], c->lxitem_cnt[L]);
         c->uitem_cnt[L] = (int64_t)uitems.size() - c->uitem_off[L];
+        mx_u = std::max(mx_u, c->uitem_cnt[L]);
+        mx_a = std::max(mx_a, c->raitem_cnt[L]);
         c->small_cnt[L] = (int64_t)small.size() - c->small_off[L];
     }
     c->item_flops.assign(nl, 0.0);
@@ -368,6 +389,20 @@ kep_status build_lists(kep_ctx* c) {
     cudaFree(c->d_xoff); c->d_xoff = nullptr;
     KEP_CUDA(c, upload(&c->d_xoff, xoff));
     c->xstride = xmax;
+    {
+        void* old[] = {c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1],
+                       c->d_rr_l[2], c->d_rr_u, c->d_rr_a};
+        for (void* q : old) cudaFree(q);
+        c->d_rr_d1 = c->d_rr_d2 = nullptr;
+        KEP_CUDA(c, upload(&c->d_rr_d1, rd1));
+        KEP_CUDA(c, upload(&c->d_rr_d2, rd2));
+        KEP_CUDA(c, cudaMalloc(&c->d_rr_fr, sizeof(int32_t) * mx_f));
+        KEP_CUDA(c, cudaMalloc(&c->d_rr_x, sizeof(int32_t) * mx_f));
+        KEP_CUDA(c, cudaMalloc(&c->d_rr_cnt, sizeof(int32_t) * 8));
+        for (int k = 0; k < 3; ++k) KEP_CUDA(c, cudaMalloc(&c->d_rr_l[k], sizeof(int4) * mx_l[k]));
+        KEP_CUDA(c, cudaMalloc(&c->d_rr_u, sizeof(int4) * mx_u));
+        KEP_CUDA(c, cudaMalloc(&c->d_rr_a, sizeof(int4) * mx_a));
+    }
     cudaFree(c->d_aitems); c->d_aitems = nullptr;
     KEP_CUDA(c, upload(&c->d_aitems, aitems));
     // pivot-record offsets: Q_s = p_s + slack entries per front
@@ -620,27 +655,64 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 // pass 0, then kReruns passes over the fronts whose full-column test failed
                 // (each with one more forced delay), then the unblocked kernel for the rest
                 const auto& groups = c->fs_groups[L];
-                int pend_q = INT_MAX;                   // rerun passes: largest flagged FS block
+                kep::RerunLists R;
+                R.d1 = c->d_rr_d1; R.d2 = c->d_rr_d2;
+                R.sl[0] = c->d_litems; R.sl[1] = c->d_lsitems; R.sl[2] = c->d_lxitems;
+                R.su = c->d_uitems; R.sa = c->d_aitems;
+                R.fr = c->d_rr_fr; R.x = c->d_rr_x; R.cnt = c->d_rr_cnt;
+                for (int k = 0; k < 3; ++k) R.l[k] = c->d_rr_l[k];
+                R.u = c->d_rr_u; R.a = c->d_rr_a;
+                int32_t rc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 for (int pass = 0; pass <= kReruns; ++pass) {
                     if (pass > 0) {                     // any front flagged for a rerun at this level?
                         int32_t pend[2] = {0, 0};
+                        mark(KEP_K_CHECK, true);
+                        kep::launch_rerun_lists(P, fl, nfl2, m, R, c->stream);
+                        mark(KEP_K_CHECK, false);
                         KEP_CUDA(c, cudaMemcpyAsync(pend, c->d_pending, sizeof(pend), cudaMemcpyDeviceToHost, c->stream));
+                        KEP_CUDA(c, cudaMemcpyAsync(rc, c->d_rr_cnt, sizeof(rc), cudaMemcpyDeviceToHost, c->stream));
                         KEP_CUDA(c, cudaStreamSynchronize(c->stream));
                         if (pend[0] == 0) break;
-                        pend_q = pend[1];
+                        // the rerun pass: flagged fronts only, one launch configuration for the largest
+                        // flagged FS block
+                        KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
+                        const int qr = std::min(pend[1], c->level_qmax[L]);
+                        const int64_t nbk = (int64_t)rc[0] * m;
+                        const int nbl = kep::front_nb_for(qr, nbk);
+                        const int iters = std::min(kep::fs_iters(qr, nbk), (qr + nbl - 2) / (nbl - 1) + 1);
+                        for (int itn = 0; itn < iters; ++itn) {
+                            mark(KEP_K_PANEL, true);
+                            kep::launch_fsp(P, c->d_rr_fr, rc[0], m, qr, itn == 0 ? 1 : 2, c->stream);
+                            mark(KEP_K_PANEL, false);
+                            c->prof.launches[KEP_K_PANEL]++;
+                            if (rc[4]) {
+                                mark(KEP_K_FSU, true);
+                                kep::launch_fsu(P, c->d_rr_u, rc[4], m, c->stream);
+                                mark(KEP_K_FSU, false);
+                                c->prof.launches[KEP_K_FSU]++;
+                            }
+                        }
+                        mark(KEP_K_L21, true);
+                        kep::launch_l21x_prep(P, c->d_rr_x, rc[6], m, c->stream);
+                        kep::launch_l21(P, c->d_rr_l[2], rc[3], m, 2, c->stream);
+                        kep::launch_l21(P, c->d_rr_l[0], rc[1], m, 0, c->stream);
+                        kep::launch_l21(P, c->d_rr_l[1], rc[2], m, 1, c->stream);
+                        mark(KEP_K_L21, false);
+                        c->prof.launches[KEP_K_L21] += 4;
+                        mark(KEP_K_CHECK, true);
+                        kep::launch_check(P, c->d_rr_fr, rc[0], m, c->stream);
+                        kep::launch_assemble(P, c->d_rr_a, rc[5], m, true, c->stream);
+                        mark(KEP_K_CHECK, false);
+                        c->prof.launches[KEP_K_CHECK] += 3;
+                        continue;
                     }
                     KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
                     for (const auto& gr : groups) {     // size groups of the level's fast fronts
                         const int64_t nbk = gr.fcnt * m;
-                        int iters = kep::fs_iters(gr.qmax, nbk);
-                        if (pass > 0) {                 // only the pivot blocks of the largest flagged FS block
-                            const int nbl = kep::front_nb_for(gr.qmax, nbk);
-                            iters = std::min(iters, (std::min(pend_q, gr.qmax) + nbl - 2) / (nbl - 1) + 1);
-                        }
+                        const int iters = kep::fs_iters(gr.qmax, nbk);
                         for (int itn = 0; itn < iters; ++itn) {
                             mark(KEP_K_PANEL, true);
-                            kep::launch_fsp(P, c->d_lists + gr.foff, (int)gr.fcnt, m, gr.qmax,
-                                            itn == 0 ? (pass == 0 ? 0 : 1) : 2, c->stream);
+                            kep::launch_fsp(P, c->d_lists + gr.foff, (int)gr.fcnt, m, gr.qmax, itn == 0 ? 0 : 2, c->stream);
                             mark(KEP_K_PANEL, false);
                             c->prof.launches[KEP_K_PANEL]++;
                             if (gr.ucnt) {
@@ -1464,7 +1536,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_level_fronts, c->d_arena_off, c->d_asm_ptr, c->d_asm_src, c->d_rmap_ptr,
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
-                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
+                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1], c->d_rr_l[2], c->d_rr_u, c->d_rr_a, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
                         c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);

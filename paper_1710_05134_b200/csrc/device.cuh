@@ -163,6 +163,18 @@ void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const dou
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, int mode, cudaStream_t st);
 int l21_mode(int qcap);              // 1: one column block (q < 32); 2: GEMM in-block solve (X scratch); 0: triangle
 int64_t l21_x_doubles(int qcap);     // X scratch of one front (k_l21x_prep)
+// compact per-pass lists of the fronts flagged for a rerun (k_rerun_lists)
+struct RerunLists {
+    const int4 *d1, *d2;         // [nf] per fast front: (l21 mode, l21 item off, cnt, uitem off), (ucnt, re-assembly off, cnt, -)
+    const int4* sl[3];           // static l21 item lists by mode
+    const int4 *su, *sa;         // static k_fsu tiles, re-assembly strips
+    int32_t* fr;                 // out: flagged fronts
+    int4* l[3];                  // out: their l21 tiles by mode
+    int4 *u, *a;                 // out: their k_fsu tiles, re-assembly strips
+    int32_t* x;                  // out: their k_l21x_prep fronts
+    int32_t* cnt;                // out [8]: fronts, l21 <0> <1> <2>, fsu, re-assembly, prep
+};
+void launch_rerun_lists(const DevPlan& P, const int32_t* fl, int n, int batch, const RerunLists& R, cudaStream_t st);
 void launch_l21x_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 int front_nb_for(int qmax, int64_t nblocks = 0);   // block width (0: too large, use the reference kernel)

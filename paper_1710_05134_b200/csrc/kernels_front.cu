@@ -952,6 +952,44 @@ __global__ void __launch_bounds__(XPW * 32) k_l21x_prep(DevPlan P, const int32_t
     }
 }
 
+// ------------------------------------------------------------------ k_rerun_lists
+// Between fast-path passes of a level (one CTA): the fronts flagged FL_RERUN in any
+// shift of the batch and their tiles of every per-front list, so the rerun pass
+// launches grids over those fronts only (≈1 % of a level) instead of the whole level.
+__global__ void __launch_bounds__(1024) k_rerun_lists(DevPlan P, const int32_t* __restrict__ fl, int n, int batch,
+                                                      RerunLists R) {
+    __shared__ int cnt[8];
+    if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int x = threadIdx.x; x < n; x += blockDim.x) {
+        const int s = fl[x];
+        bool fg = false;
+        for (int sh = 0; sh < batch; ++sh) fg |= P.flag[(size_t)sh * P.nf + s] == FL_RERUN;
+        if (!fg) continue;
+        const int4 a = R.d1[s], b = R.d2[s];           // (l21 mode, l21 off, l21 cnt, uitem off), (ucnt, aoff, acnt, -)
+        int k = atomicAdd(&cnt[0], 1);
+        R.fr[k] = s;
+        if (a.z > 0) {
+            k = atomicAdd(&cnt[1 + a.x], a.z);
+            for (int i = 0; i < a.z; ++i) R.l[a.x][k + i] = R.sl[a.x][a.y + i];
+        }
+        if (b.x > 0) {
+            k = atomicAdd(&cnt[4], b.x);
+            for (int i = 0; i < b.x; ++i) R.u[k + i] = R.su[a.w + i];
+        }
+        if (b.z > 0) {
+            k = atomicAdd(&cnt[5], b.z);
+            for (int i = 0; i < b.z; ++i) R.a[k + i] = R.sa[b.y + i];
+        }
+        if (a.x == 2) {
+            k = atomicAdd(&cnt[6], 1);
+            R.x[k] = s;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) R.cnt[threadIdx.x] = cnt[threadIdx.x];
+}
+
 // ------------------------------------------------------------------ k_check
 __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restrict__ fronts) {
     __shared__ int s_ok;
@@ -1175,6 +1213,10 @@ void launch_l21x_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int 
     static bool attr = false;
     if (!attr) { cudaFuncSetAttribute(k_l21x_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
     k_l21x_prep<<<dim3(nfronts, batch), XPW * 32, smem, st>>>(P, fronts);
+}
+
+void launch_rerun_lists(const DevPlan& P, const int32_t* fl, int n, int batch, const RerunLists& R, cudaStream_t st) {
+    k_rerun_lists<<<1, 1024, 0, st>>>(P, fl, n, batch, R);
 }
 
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
