@@ -78,6 +78,7 @@ struct kep_ctx {
     std::vector<std::vector<FsGroup>> fs_groups;   // per level: fast fronts by FS capacity (k_fsp/k_fsu passes)
     int4* d_aitems = nullptr;                   // k_assemble strips (front, x, S, 0): all fronts, then fast fronts
     std::vector<int64_t> aitem_off, aitem_cnt, raitem_off, raitem_cnt;
+    std::vector<char> asm_red;                  // per level: small fronts, k_assemble_red
     std::vector<int64_t> fast_off, fast_cnt, ref_off, ref_cnt, item_off, item_cnt, litem_off, litem_cnt;
     // fast-path pivot records: per-front offsets (entries), per shift stride (doubles)
     int64_t* d_aux_off = nullptr;
@@ -209,17 +210,12 @@ kep_status alloc_batch(kep_ctx* c) {
 // tiles) and fronts for the reference kernel; build the Schur work items.
 kep_status build_lists(kep_ctx* c) {
     const Symbolic& S = c->sym;
-    // fast (blocked) path, or the unblocked kernel (variant 1, and tiny fronts whose whole
-    // factorisation fits one CTA's worth of work)
+    // fast (blocked) path, or the unblocked kernel (variant 1; FS blocks beyond the fast kernels)
+    // (routing tiny fronts to the unblocked kernel measured slower at c4: its fronts live in HBM)
     auto is_fast = [&](int s) {
-        const int qcap = S.capacity[s] - S.ncb[s];
-        if (c->opts.kernel_variant != 0 || kep::front_nb_for(qcap) <= 0) return false;
-        const char* e = getenv("KEP_TINY_REF");
-        const int tiny = e ? atoi(e) : 0;
-        return !(qcap <= tiny && S.ncb[s] <= 4 * tiny);
+        return c->opts.kernel_variant == 0 && kep::front_nb_for(S.capacity[s] - S.ncb[s]) > 0;
     };
     const int nl = (int)S.level_ptr.size() - 1;
-    const bool use_fast = c->opts.kernel_variant == 0;
     std::vector<int32_t> fast, ref;
     std::vector<int4> items, litems, lsitems, lxitems, uitems;
     std::vector<int32_t> xfronts;
@@ -246,6 +242,7 @@ kep_status build_lists(kep_ctx* c) {
     c->ref_off.assign(nl, 0); c->ref_cnt.assign(nl, 0);
     c->item_off.assign(nl, 0); c->item_cnt.assign(nl, 0);
     c->level_qmax.assign(nl, 0);
+    c->asm_red.assign(nl, 0);
     c->fs_groups.clear();
     for (int L = 0; L < nl; ++L) {
         c->fast_off[L] = (int64_t)fast.size();
@@ -259,6 +256,12 @@ kep_status build_lists(kep_ctx* c) {
         c->uitem_off[L] = (int64_t)uitems.size();
         c->small_off[L] = (int64_t)small.size();
         c->aitem_off[L] = (int64_t)aitems.size();
+        {   // small-front levels: whole-front RED assembly (measured faster below ~700 at c4)
+            double sf = 0.0;
+            for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) sf += S.forder[S.level_fronts[k]];
+            const int nlf = S.level_ptr[L + 1] - S.level_ptr[L];
+            c->asm_red[L] = nlf > 0 && sf / nlf < 700.0;
+        }
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) strips(S.level_fronts[k], INT_MAX);
         c->aitem_cnt[L] = (int64_t)aitems.size() - c->aitem_off[L];
         c->raitem_off[L] = (int64_t)aitems.size();
@@ -646,7 +649,8 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
         for (int L = 0; L < nl; ++L) {
             const int b = S.level_ptr[L], nfl = S.level_ptr[L + 1] - b;
             mark(KEP_K_ASSEMBLE, true);
-            kep::launch_assemble(P, c->d_aitems + c->aitem_off[L], (int)c->aitem_cnt[L], m, false, c->stream);
+            if (c->asm_red[L]) kep::launch_assemble_red(P, c->d_level_fronts + b, nfl, m, c->stream);
+            else kep::launch_assemble(P, c->d_aitems + c->aitem_off[L], (int)c->aitem_cnt[L], m, false, c->stream);
             mark(KEP_K_ASSEMBLE, false);
             c->prof.launches[KEP_K_ASSEMBLE]++;
             if (c->fast_cnt[L]) {

@@ -406,6 +406,162 @@ __global__ void __launch_bounds__(kAsmThreads, 4) k_reassemble(DevPlan P, const 
     }
 }
 
+// ---------------------------------------------------------------- a1 + a2, small fronts
+// Levels of small fronts (short columns: the gather form's per-column child searches
+// dominate there): whole-front CTAs (S per front when the level is small), zero-fill,
+// stores, then the children's entries with fire-and-forget RED adds, children in order.
+constexpr int kAsmRedThreads = 256;
+constexpr int kAsmRedMapMax = 8192;       // child CB positions staged in shared memory
+
+// One front of a level, S CTAs per front (blockIdx.x = front * S + x): CTA x
+// owns the parent columns [lo, hi): zero-fill, original entries (alpha a - sigma b),
+// then the children's CB entries landing in those columns, children in order.
+// Each parent entry belongs to one CTA, so the sum order is fixed (deterministic).
+__device__ __forceinline__ void assemble_front_red(const DevPlan& P, const int32_t* __restrict__ list, int S,
+                                               int only_flagged) {
+    const int s = list[blockIdx.x / S];
+    const int xs = blockIdx.x % S;
+    const int sh = blockIdx.y;
+    if (only_flagged) {               // re-assembly of fronts whose fast-path pass failed (restore)
+        const int fl = P.flag[(size_t)sh * P.nf + s];
+        if (fl != FL_RERUN && fl != FL_REF) return;
+    }
+    ShiftStat* st = P.stats + sh;
+    double* arena = P.arena + (size_t)sh * P.arena_stride;
+    int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
+    const int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
+    int32_t* doff = P.doff + (size_t)sh * P.nf;
+    __shared__ int s_nd, s_skip;
+    __shared__ double s_red[32];
+    __shared__ int s_pos[kAsmRedMapMax];
+    const int c0 = P.child_ptr[s], c1 = P.child_ptr[s + 1];
+    if (threadIdx.x == 0) {
+        int off = 0, bad = 0;
+        for (int q = c0; q < c1; ++q) {
+            const int c = P.child_list[q];
+            const int no = nd_out[c];
+            if (no < 0) bad = 1;
+            if (xs == 0) doff[c] = off;
+            off += no > 0 ? no : 0;
+        }
+        const int need = P.forder[s] + off;
+        if (need > P.cap[s]) {
+            bad = 1;
+            if (xs == 0) atomicMax(&st->need_slack, off);
+        }
+        if (bad && xs == 0) atomicOr(&st->flags, FLAG_OVERFLOW);
+        s_skip = bad;
+        s_nd = off;
+        if (xs == 0) nd_in[s] = bad ? -1 : off;
+    }
+    __syncthreads();
+    if (s_skip) return;
+    const int nd = s_nd, p = P.npiv[s], fo = P.forder[s] + nd, ld = ldpad(fo);   // order, leading dimension
+    double* F = arena + P.arena_off[s];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAsmRedThreads / 32;
+    int clo, chi;
+    tri_split(fo, S, xs, clo, chi);
+    if (xs == 0) {   // labels of the FS positions: own pivots, then each child's delayed variables
+        const AuxRec A = aux_rec(P, sh, s, P.cap[s] - P.ncb[s]);
+        for (int i = threadIdx.x; i < p; i += kAsmRedThreads) A.label[i] = P.piv_first[s] + i;
+        int off = 0;
+        for (int q = c0; q < c1; ++q) {
+            const int c = P.child_list[q];
+            const int ndo = nd_out[c];
+            if (ndo <= 0) continue;
+            const AuxRec C = aux_rec(P, sh, c, P.cap[c] - P.ncb[c]);
+            const int ec = P.npiv[c] + nd_in[c] - ndo;
+            for (int j = threadIdx.x; j < ndo; j += kAsmRedThreads) A.label[p + off + j] = C.label[C.perm[ec + j]];
+            off += ndo;
+        }
+    }
+    for (int j = clo + warp; j < chi; j += nw)
+        for (int i = j + lane; i < fo; i += 32) F[i + (size_t)j * ld] = 0.0;
+    __syncthreads();
+    const double sigma = P.sigma[sh], alpha = P.alpha[sh];
+    double mx = 0.0;
+    for (int64_t k = P.asm_ptr[s] + threadIdx.x; k < P.asm_ptr[s + 1]; k += kAsmRedThreads) {
+        const uint32_t rc = P.asm_rc[k];
+        const int lr = (int)(rc >> 16), lc = (int)(rc & 0xffffu);
+        if (lc < clo || lc >= chi) continue;
+        const int r = lr < p ? lr : lr + nd;
+        const double v = fma(-sigma, P.b[k], alpha * P.a[k]);      // alpha A - sigma B (alpha = 1: A - sigma B)
+        F[r + (size_t)lc * ld] = v;
+        mx = fmax(mx, fabs(v));
+    }
+    mx = block_max<kAsmRedThreads>(mx, s_red);
+    if (threadIdx.x == 0 && mx > 0.0) atomic_max_pos_double(&st->smax_bits, mx);
+    // a2: extend-add, children in a fixed order
+    int off = 0;
+    for (int q = c0; q < c1; ++q) {
+        const int c = P.child_list[q];
+        const int ndo = nd_out[c];
+        const int fc = P.forder[c] + nd_in[c];       // child order
+        const int ldc = ldpad(fc);                   // child leading dimension
+        const int mc = ndo + P.ncb[c];
+        const int ec = fc - mc;
+        const double* __restrict__ Fc = arena + P.arena_off[c];
+        double* __restrict__ Fp = F;
+        // fast-path children keep the CB rows of their delayed columns in W21 (upper part)
+        const bool wup = P.flag[(size_t)sh * P.nf + c] == FL_OK && ndo > 0;
+        const int32_t* __restrict__ rm = P.rmap + P.rmap_ptr[c];
+        const int dof = p + off;
+        off += ndo > 0 ? ndo : 0;
+        const bool staged = mc <= kAsmRedMapMax;
+        __syncthreads();                                         // s_pos reuse
+        if (staged)
+            for (int x = threadIdx.x; x < mc; x += kAsmRedThreads) {
+                int v;
+                if (x < ndo) v = dof + x;
+                else { const int r = rm[x - ndo]; v = r < p ? r : r + nd; }
+                s_pos[x] = v;
+            }
+        __syncthreads();
+        auto pos = [&](int x) -> int {
+            if (staged) return s_pos[x];
+            if (x < ndo) return dof + x;
+            const int r = rm[x - ndo];
+            return r < p ? r : r + nd;
+        };
+        constexpr int U = 4;                                     // rows in flight per lane
+        for (int j = warp; j < mc; j += nw) {
+            const int pj = pos(j);
+            // non-delayed child columns land in parent column pj (positions increase with the
+            // child index there); delayed columns are filtered entry by entry
+            if (j >= ndo && (pj < clo || pj >= chi)) continue;
+            const double* __restrict__ colc = Fc + (size_t)(ec + j) * ldc + ec;
+            for (int i0 = j; i0 < mc; i0 += 32 * U) {
+                double v[U];
+                size_t dst[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + lane + 32 * u;
+                    dst[u] = SIZE_MAX;
+                    v[u] = 0.0;
+                    if (i < mc) {
+                        const int pi = pos(i);
+                        const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
+                        if (lo >= clo && lo < chi) {
+                            dst[u] = hi + (size_t)lo * ld;
+                            v[u] = (wup && j < ndo && i >= ndo) ? Fc[(ec + j) + (size_t)(ec + i) * ldc] : colc[i];
+                        }
+                    }
+                }
+                // one writer per parent entry and child (children ordered by the barrier
+                // between them): fire-and-forget RED adds, no load latency
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (dst[u] != SIZE_MAX) atomicAdd(&Fp[dst[u]], v[u]);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kAsmRedThreads) k_assemble_red(DevPlan P, const int32_t* __restrict__ list, int S) {
+    assemble_front_red(P, list, S, 0);
+}
+
+
 // ---------------------------------------------------------------- a3 + a4 + a5 (reference)
 constexpr int kRefThreads = 256;
 
@@ -633,6 +789,14 @@ void launch_assemble(const DevPlan& P, const int4* items, int nitems, int batch,
 int assembly_strips(int forder) {
     const int64_t T = (int64_t)forder * (forder + 1) / 2;
     return (int)std::max<int64_t>(1, (T + kAsmStripEnt - 1) / kAsmStripEnt);
+}
+
+void launch_assemble_red(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    // CTAs per front: enough to give ~4 resident CTAs per SM on the whole level
+    int S = (int)((4 * 148 + (int64_t)nfronts * batch - 1) / ((int64_t)nfronts * batch));
+    S = std::max(1, std::min(S, 16));
+    k_assemble_red<<<dim3(nfronts * S, batch), kAsmRedThreads, 0, st>>>(P, fronts, S);
 }
 
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,
