@@ -667,17 +667,40 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 for (int k = 0; k < 3; ++k) R.l[k] = c->d_rr_l[k];
                 R.u = c->d_rr_u; R.a = c->d_rr_a;
                 int32_t rc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                int32_t pend[2] = {0, 0};
+                KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
                 for (int pass = 0; pass <= kReruns; ++pass) {
-                    if (pass > 0) {                     // any front flagged for a rerun at this level?
-                        int32_t pend[2] = {0, 0};
+                    if (pass == 0) {
+                        for (const auto& gr : groups) { // size groups of the level's fast fronts
+                            const int64_t nbk = gr.fcnt * m;
+                            const int iters = kep::fs_iters(gr.qmax, nbk);
+                            for (int itn = 0; itn < iters; ++itn) {
+                                mark(KEP_K_PANEL, true);
+                                kep::launch_fsp(P, c->d_lists + gr.foff, (int)gr.fcnt, m, gr.qmax, itn == 0 ? 0 : 2, c->stream);
+                                mark(KEP_K_PANEL, false);
+                                c->prof.launches[KEP_K_PANEL]++;
+                                if (gr.ucnt) {
+                                    mark(KEP_K_FSU, true);
+                                    kep::launch_fsu(P, c->d_uitems + gr.uoff, (int)gr.ucnt, m, c->stream);
+                                    mark(KEP_K_FSU, false);
+                                    c->prof.launches[KEP_K_FSU]++;
+                                }
+                            }
+                        }
+                        if (c->litem_cnt[L] || c->lsitem_cnt[L] || c->lxitem_cnt[L]) {
+                            mark(KEP_K_L21, true);
+                            kep::launch_l21x_prep(P, c->d_xfronts + c->xfront_off[L], (int)c->xfront_cnt[L], m, c->stream);
+                            kep::launch_l21(P, c->d_lxitems + c->lxitem_off[L], (int)c->lxitem_cnt[L], m, 2, c->stream);
+                            kep::launch_l21(P, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, 0, c->stream);
+                            kep::launch_l21(P, c->d_lsitems + c->lsitem_off[L], (int)c->lsitem_cnt[L], m, 1, c->stream);
+                            mark(KEP_K_L21, false);
+                            c->prof.launches[KEP_K_L21] += 2 * (c->lxitem_cnt[L] > 0) + (c->litem_cnt[L] > 0) + (c->lsitem_cnt[L] > 0);
+                        }
                         mark(KEP_K_CHECK, true);
-                        kep::launch_rerun_lists(P, fl, nfl2, m, R, c->stream);
+                        kep::launch_check(P, fl, nfl2, m, c->stream);
                         mark(KEP_K_CHECK, false);
-                        KEP_CUDA(c, cudaMemcpyAsync(pend, c->d_pending, sizeof(pend), cudaMemcpyDeviceToHost, c->stream));
-                        KEP_CUDA(c, cudaMemcpyAsync(rc, c->d_rr_cnt, sizeof(rc), cudaMemcpyDeviceToHost, c->stream));
-                        KEP_CUDA(c, cudaStreamSynchronize(c->stream));
-                        if (pend[0] == 0) break;
-                        // the rerun pass: flagged fronts only, one launch configuration for the largest
+                    } else {
+                        // rerun pass: the flagged fronts only, one launch configuration for the largest
                         // flagged FS block
                         KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
                         const int qr = std::min(pend[1], c->level_qmax[L]);
@@ -705,48 +728,29 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                         c->prof.launches[KEP_K_L21] += 4;
                         mark(KEP_K_CHECK, true);
                         kep::launch_check(P, c->d_rr_fr, rc[0], m, c->stream);
-                        kep::launch_assemble(P, c->d_rr_a, rc[5], m, true, c->stream);
                         mark(KEP_K_CHECK, false);
-                        c->prof.launches[KEP_K_CHECK] += 3;
-                        continue;
                     }
-                    KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
-                    for (const auto& gr : groups) {     // size groups of the level's fast fronts
-                        const int64_t nbk = gr.fcnt * m;
-                        const int iters = kep::fs_iters(gr.qmax, nbk);
-                        for (int itn = 0; itn < iters; ++itn) {
-                            mark(KEP_K_PANEL, true);
-                            kep::launch_fsp(P, c->d_lists + gr.foff, (int)gr.fcnt, m, gr.qmax, itn == 0 ? 0 : 2, c->stream);
-                            mark(KEP_K_PANEL, false);
-                            c->prof.launches[KEP_K_PANEL]++;
-                            if (gr.ucnt) {
-                                mark(KEP_K_FSU, true);
-                                kep::launch_fsu(P, c->d_uitems + gr.uoff, (int)gr.ucnt, m, c->stream);
-                                mark(KEP_K_FSU, false);
-                                c->prof.launches[KEP_K_FSU]++;
-                            }
-                        }
-                    }
-                    if (c->litem_cnt[L] || c->lsitem_cnt[L] || c->lxitem_cnt[L]) {
-                        mark(KEP_K_L21, true);
-                        kep::launch_l21x_prep(P, c->d_xfronts + c->xfront_off[L], (int)c->xfront_cnt[L], m, c->stream);
-                        kep::launch_l21(P, c->d_lxitems + c->lxitem_off[L], (int)c->lxitem_cnt[L], m, 2, c->stream);
-                        kep::launch_l21(P, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, 0, c->stream);
-                        kep::launch_l21(P, c->d_lsitems + c->lsitem_off[L], (int)c->lsitem_cnt[L], m, 1, c->stream);
-                        mark(KEP_K_L21, false);
-                        c->prof.launches[KEP_K_L21] += 2 * (c->lxitem_cnt[L] > 0) + (c->litem_cnt[L] > 0) + (c->lsitem_cnt[L] > 0);
-                    }
+                    // fronts whose full-column test failed: compact lists, restore by re-assembly
                     mark(KEP_K_CHECK, true);
-                    kep::launch_check(P, fl, nfl2, m, c->stream);
-                    // restore failed fronts: assemble again
-                    kep::launch_assemble(P, c->d_aitems + c->raitem_off[L], (int)c->raitem_cnt[L], m, true, c->stream);
+                    kep::launch_rerun_lists(P, fl, nfl2, m, R, c->stream);
                     mark(KEP_K_CHECK, false);
-                    c->prof.launches[KEP_K_CHECK] += 3;
+                    KEP_CUDA(c, cudaMemcpyAsync(pend, c->d_pending, sizeof(pend), cudaMemcpyDeviceToHost, c->stream));
+                    KEP_CUDA(c, cudaMemcpyAsync(rc, c->d_rr_cnt, sizeof(rc), cudaMemcpyDeviceToHost, c->stream));
+                    KEP_CUDA(c, cudaStreamSynchronize(c->stream));
+                    c->prof.launches[KEP_K_CHECK] += 2;
+                    if (rc[5] == 0) break;              // nothing flagged
+                    mark(KEP_K_CHECK, true);
+                    kep::launch_assemble(P, c->d_rr_a, rc[5], m, true, c->stream);
+                    mark(KEP_K_CHECK, false);
+                    c->prof.launches[KEP_K_CHECK]++;
+                    if (rc[0] == 0) break;              // only fronts for the unblocked kernel
                 }
-                mark(KEP_K_REF, true);
-                kep::launch_factor_list(P, fl, nfl2, m, c->stream, true);
-                mark(KEP_K_REF, false);
-                c->prof.launches[KEP_K_REF]++;
+                if (rc[5] > 0) {                        // fronts left for the unblocked kernel
+                    mark(KEP_K_REF, true);
+                    kep::launch_factor_list(P, fl, nfl2, m, c->stream, true);
+                    mark(KEP_K_REF, false);
+                    c->prof.launches[KEP_K_REF]++;
+                }
             }
             if (c->ref_cnt[L]) {
                 mark(KEP_K_REF, true);

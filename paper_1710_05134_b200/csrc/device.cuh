@@ -169,7 +169,7 @@ struct RerunLists {
     const int4 *d1, *d2;         // [nf] per fast front: (l21 mode, l21 item off, cnt, uitem off), (ucnt, re-assembly off, cnt, -)
     const int4* sl[3];           // static l21 item lists by mode
     const int4 *su, *sa;         // static k_fsu tiles, re-assembly strips
-    int32_t* fr;                 // out: flagged fronts
+    int32_t* fr;                 // out: fronts flagged FL_RERUN (re-assembly strips: FL_RERUN or FL_REF)
     int4* l[3];                  // out: their l21 tiles by mode
     int4 *u, *a;                 // out: their k_fsu tiles, re-assembly strips
     int32_t* x;                  // out: their k_l21x_prep fronts

@@ -963,11 +963,21 @@ __global__ void __launch_bounds__(1024) k_rerun_lists(DevPlan P, const int32_t* 
     __syncthreads();
     for (int x = threadIdx.x; x < n; x += blockDim.x) {
         const int s = fl[x];
-        bool fg = false;
-        for (int sh = 0; sh < batch; ++sh) fg |= P.flag[(size_t)sh * P.nf + s] == FL_RERUN;
-        if (!fg) continue;
+        bool fg = false, fa = false;                    // flagged for a rerun / for a rerun or the unblocked kernel
+        for (int sh = 0; sh < batch; ++sh) {
+            const int32_t v = P.flag[(size_t)sh * P.nf + s];
+            fg |= v == FL_RERUN;
+            fa |= v == FL_RERUN || v == FL_REF;
+        }
+        if (!fa) continue;
         const int4 a = R.d1[s], b = R.d2[s];           // (l21 mode, l21 off, l21 cnt, uitem off), (ucnt, aoff, acnt, -)
-        int k = atomicAdd(&cnt[0], 1);
+        int k;
+        if (b.z > 0) {                                  // re-assembly (restore) of every flagged front
+            k = atomicAdd(&cnt[5], b.z);
+            for (int i = 0; i < b.z; ++i) R.a[k + i] = R.sa[b.y + i];
+        }
+        if (!fg) continue;
+        k = atomicAdd(&cnt[0], 1);
         R.fr[k] = s;
         if (a.z > 0) {
             k = atomicAdd(&cnt[1 + a.x], a.z);
@@ -976,10 +986,6 @@ __global__ void __launch_bounds__(1024) k_rerun_lists(DevPlan P, const int32_t* 
         if (b.x > 0) {
             k = atomicAdd(&cnt[4], b.x);
             for (int i = 0; i < b.x; ++i) R.u[k + i] = R.su[a.w + i];
-        }
-        if (b.z > 0) {
-            k = atomicAdd(&cnt[5], b.z);
-            for (int i = 0; i < b.z; ++i) R.a[k + i] = R.sa[b.y + i];
         }
         if (a.x == 2) {
             k = atomicAdd(&cnt[6], 1);
