@@ -56,7 +56,7 @@ constexpr int LB = 32;                          // k_l21 column block
 constexpr int LST = 3;                          // k_l21 cp.async pipeline depth
 static_assert(LT == 8 * LB, "k_l21 column-max reduction maps 8 threads to a column");
 constexpr int KC = 16;                          // K chunk of the k_l21 GEMM
-constexpr int kXMin = 64;                       // k_l21<2> (GEMM in-block solve) from this FS capacity
+constexpr int kXMin = 48;                       // k_l21<2> (GEMM in-block solve) from this FS capacity (c4 sweep 32/48/56/64)
 constexpr int kXMaxBlocks = 256;                // ... up to this many column blocks
 constexpr int XPW = 4;                          // k_l21x_prep warps per CTA
 constexpr int APAD = LR + 4;                    // = 4 (mod 16): conflict-free f64 fragments
