@@ -92,8 +92,10 @@ enum { KEP_K_ASSEMBLE = 0,   /* a1 + a2: assembly + extend-add */
        KEP_K_REF = 2,        /* a3 + a4 + a5: reference unblocked front factorisation (variant 1, fronts
                                 too large for the fast path, fronts that failed the full-column test) */
        KEP_K_SCHUR = 3,      /* a4: DMMA contribution-block update */
-       KEP_K_L21 = 4,        /* a3: CB rows of the FS columns, W21 = A21 P^T L11^-T (k_l21) */
-       KEP_K_CHECK = 5,      /* a3 + a5: full-column threshold tests, inertia, D^-1 coefficients */
+       KEP_K_L21 = 4,        /* a3: CB rows of the FS columns, G21 = W21 D^-1 M, W21 = A21 P^T L11^-T
+                                (k_l21x_prep, k_l21) */
+       KEP_K_CHECK = 5,      /* a3 + a5: full-column threshold tests, inertia, rerun lists, re-assembly of
+                                fronts that failed them */
        KEP_K_FSU = 6,        /* a3: FS x FS trailing update after each pivot block (k_fsu) */
        KEP_K_NCLASS = 7 };
 
