@@ -26,7 +26,11 @@ about its internals; this oracle takes the readings listed in DESIGN.md:
   complement C - L21 D L21^T (one matmul), passed to the parent together
   with the delayed rows/columns.
 
-Plain numpy, fp64, unblocked pivot loop, full symmetric dense fronts.
+Plain numpy, fp64, full symmetric dense fronts; the pivot loop is unblocked
+(_partial_fs_bk, the default) or, for the large configurations, the same rule
+with nb-column panels and a BLAS3 update of the remaining FS columns
+(_partial_fs_bk_blocked, pinned against the unblocked loop and eigh in
+tests/test_oracle.py).
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 """
 from __future__ import annotations
@@ -182,7 +186,10 @@ class SparseOracle:
                [self.struct[b].shape[0] * self.o for b in range(len(self.blocks))]
 
     # ------------------------------------------------------------------------- numeric
-    def inertia(self, sigma: float, u: float = U_THRESHOLD) -> Inertia:
+    def inertia(self, sigma: float, u: float = U_THRESHOLD, nb: int = 0) -> Inertia:
+        """Inertia of D.  nb = 0: the unblocked pivot loop (_partial_fs_bk);
+        nb >= 1: the same pivot rule with nb-column panels and a BLAS3 update of
+        the remaining FS columns after each panel (_partial_fs_bk_blocked)."""
         p = self.p
         vals = (p.a - sigma * p.b)[self.e_src]
         total = Inertia(smax=float(np.max(np.abs(vals))) if vals.shape[0] else 0.0)
@@ -201,7 +208,7 @@ class SparseOracle:
             idx = np.concatenate([fs, rest])
             f = idx.shape[0]
             pos[idx] = np.arange(f)
-            F = np.zeros((f, f))
+            F = np.zeros((f, f), order="F" if nb > 0 else "C")
             # assemble original entries of the pivot columns (lower part, rows >= col)
             lo, hi = self.e_colptr[piv[0]], self.e_colptr[piv[-1] + 1]
             r = pos[self.e_row[lo:hi]]
@@ -218,7 +225,10 @@ class SparseOracle:
                 assert np.all(li >= 0)
                 F[np.ix_(li, li)] += C
             root = rest.shape[0] == 0
-            inert, order, e_cnt = _partial_fs_bk(F, fs.shape[0], u=u, root=root)
+            if nb > 0:
+                inert, order, e_cnt = _partial_fs_bk_blocked(F, fs.shape[0], u=u, root=root, nb=nb)
+            else:
+                inert, order, e_cnt = _partial_fs_bk(F, fs.shape[0], u=u, root=root)
             total.add(inert)
             if not root:
                 loc = order[e_cnt:]
@@ -335,6 +345,172 @@ def _partial_fs_bk(F: np.ndarray, nfs: int, u: float, root: bool):
         for (k, sz, Dk) in Dblocks:
             W[:, k:k + sz] = L21[:, k:k + sz] @ Dk
         F[q:, q:] -= W @ L21.T
+    if e < f:
+        T = F[e:, e:]
+        lowT = np.tril(T)
+        F[e:, e:] = lowT + np.tril(lowT, -1).T
+    return res, order, e
+
+
+def _partial_fs_bk_blocked(F: np.ndarray, nfs: int, u: float, root: bool, nb: int = 64):
+    """The pivot rule of _partial_fs_bk with the FS columns eliminated in panels.
+
+    Same contract and the same pivot sequence in exact arithmetic (SURVEY.md
+    §8(c) O-sparse step 3: "nb-column BK panels with a BLAS3 update of the
+    remaining FS columns"; the LAPACK dsytf2 -> dlasyf idea).  Inside a panel
+    F is not updated: the current value of column j is formed on demand as
+        F[:, j] - Lp[:, :t] Wp[j, :t]^T,     Lp = L columns, Wp = L D columns
+    of the t pivots eliminated since the panel started (a 1x1 pivot d with
+    updated column v contributes L = v / d, W = v; a 2x2 block Dk with updated
+    columns V contributes L = V Dk^-1, W = V).  Every decision (BK choice,
+    threshold test, delay) reads only such on-demand columns, exactly the
+    values the unblocked loop holds at that step.  When the panel holds >= nb
+    pivots (or no candidate is left) the remaining FS columns are updated at
+    once: F[e:, e:q] -= Lp[e:] Wp[e:q]^T.  Rows and columns are swapped in F,
+    Lp and Wp together, so swaps commute with the pending update.  With nb = 1
+    every panel holds one pivot and this is the unblocked loop.
+
+    Only the CB rows (>= q, never swapped) of L are kept for the final Schur
+    complement, so a root front needs no L storage.
+    """
+    f = F.shape[0]
+    q = nfs
+    res = Inertia()
+    order = np.arange(f)
+    L21 = np.zeros((f - q, q))              # multipliers of the CB rows (rows >= q)
+    Dblocks = []
+    e = 0
+    qe = q
+    width = nb + 1                          # a 2x2 pivot may overfill the panel by one column
+    Lp = np.zeros((f, width), order="F")
+    Wp = np.zeros((f, width), order="F")
+    t = 0
+
+    def col(j):                             # current column j, rows e..f-1
+        c = F[e:, j].copy()
+        if t:
+            c -= Lp[e:, :t] @ Wp[j, :t]
+        return c
+
+    def swap(i, j):
+        if i == j:
+            return
+        F[[i, j], :] = F[[j, i], :]
+        F[:, [i, j]] = F[:, [j, i]]
+        Lp[[i, j], :t] = Lp[[j, i], :t]
+        Wp[[i, j], :t] = Wp[[j, i], :t]
+        order[[i, j]] = order[[j, i]]
+
+    def flush():
+        nonlocal t
+        if t and e < q:
+            F[e:, e:q] -= Lp[e:, :t] @ Wp[e:q, :t].T
+        t = 0
+
+    while e < qe:
+        k = e
+        ck = col(k)                          # ck[i - k] = current F[i, k]
+        akk = abs(ck[0])
+        candC = np.abs(ck[1:qe - k])
+        if candC.shape[0]:
+            r = k + 1 + int(np.argmax(candC))
+            gC = float(candC[r - k - 1])
+        else:
+            r, gC = k, 0.0
+        gR = float(np.max(np.abs(ck[1:]))) if f - k > 1 else 0.0
+        if akk == 0.0 and gR == 0.0:
+            res.n_zero += 1                   # zero column: exact zero pivot, nothing to update
+            res.min_abs_pivot = 0.0
+            Dblocks.append((k, 1, np.zeros((1, 1))))
+            e += 1
+            if e >= qe:
+                flush()
+            continue
+        cr = None
+        if akk >= ALPHA * gC:
+            kind, j = 1, k
+        else:
+            cr = col(r)                       # cr[i - k] = current F[i, r]
+            rowr = np.abs(cr[0:qe - k])
+            rowr[r - k] = 0.0
+            rho = float(np.max(rowr))
+            if akk * rho >= ALPHA * gC * gC:
+                kind, j = 1, k
+            elif abs(cr[r - k]) >= ALPHA * rho:
+                kind, j = 1, r
+            else:
+                kind, j = 2, r
+        if not root:
+            if kind == 1:
+                cj = ck if j == k else cr
+                colj = np.abs(cj)
+                colj[j - k] = 0.0
+                ok = abs(cj[j - k]) >= u * float(np.max(colj))
+            else:
+                fkk, frr, frk = ck[0], cr[r - k], ck[r - k]
+                det = fkk * frr - frk * frk
+                if det == 0.0:
+                    ok = False
+                else:
+                    gk = np.abs(ck); gk[0] = 0.0; gk[r - k] = 0.0
+                    gr = np.abs(cr); gr[0] = 0.0; gr[r - k] = 0.0
+                    Dinv = np.abs(np.array([[frr, -frk], [-frk, fkk]]) / det)
+                    tt = Dinv @ np.array([float(np.max(gk)), float(np.max(gr))])
+                    ok = bool(np.all(tt <= 1.0 / u))
+            if not ok:
+                swap(k, qe - 1)             # delay column k to the parent
+                qe -= 1
+                res.n_delayed += 1
+                if e >= qe:
+                    flush()
+                continue
+        if kind == 1:
+            swap(k, j)
+            ck = col(k)
+            d = ck[0]
+            v = ck[1:]
+            Lp[k + 1:, t] = v / d
+            Wp[k + 1:, t] = v
+            Lp[:k + 1, t] = 0.0
+            Wp[:k + 1, t] = 0.0
+            if q < f:
+                L21[:, k] = v[q - k - 1:] / d
+            Dblocks.append((k, 1, np.array([[d]])))
+            neg, zer, pos, mn = block_inertia_1x1(d)
+            t += 1
+            e += 1
+        else:
+            swap(k + 1, r)
+            c0 = col(k)
+            c1 = col(k + 1)
+            Dk = np.array([[c0[0], c1[0]], [c1[0], c1[1]]])
+            V = np.stack([c0[2:], c1[2:]], axis=1)
+            W = V @ np.linalg.inv(Dk)
+            Lp[k + 2:, t:t + 2] = W
+            Wp[k + 2:, t:t + 2] = V
+            Lp[:k + 2, t:t + 2] = 0.0
+            Wp[:k + 2, t:t + 2] = 0.0
+            if q < f:
+                L21[:, k:k + 2] = W[q - k - 2:]
+            Dblocks.append((k, 2, Dk))
+            neg, zer, pos, mn = block_inertia_2x2(Dk[0, 0], Dk[1, 0], Dk[1, 1])
+            res.n_2x2 += 1
+            t += 2
+            e += 2
+        res.n_neg += neg
+        res.n_zero += zer
+        res.n_pos += pos
+        res.min_abs_pivot = min(res.min_abs_pivot, mn)
+        if t >= nb or e >= qe:
+            flush()
+    flush()
+    if q < f and e > 0:
+        # Schur complement of the non-FS block: C -= L21 D L21^T
+        L = L21[:, :e]
+        W = np.zeros_like(L)
+        for (k, sz, Dk) in Dblocks:
+            W[:, k:k + sz] = L[:, k:k + sz] @ Dk
+        F[q:, q:] -= W @ L.T
     if e < f:
         T = F[e:, e:]
         lowT = np.tril(T)

@@ -61,7 +61,10 @@ class Multisection:
         P = self.world * self.shifts_per_rank
         return b.lo + (np.arange(P, dtype=np.float64) + 1.0) * (b.hi - b.lo) / (P + 1)
 
-    def _local(self, sig: np.ndarray, width: float) -> np.ndarray:
+    def _local(self, sig: np.ndarray, width: float):
+        """nu at this rank's shifts; a singular shift is moved by attempt * 1e-6 * width
+        and re-evaluated (R3).  Returns (nus, shifts actually evaluated)."""
+        sig = np.asarray(sig, dtype=np.float64).copy()
         nus, st = self.nu_many(sig)
         nus = np.asarray(nus, dtype=np.int64).copy()
         st = np.asarray(st)
@@ -76,27 +79,38 @@ class Multisection:
                     break
             else:
                 raise RuntimeError(f"shift {s} stays singular after perturbation")
-        return nus
+        return nus, sig
 
-    def _allgather(self, local: np.ndarray) -> np.ndarray:
+    def _allgather(self, nus: np.ndarray, sig: np.ndarray):
+        """All ranks' (nu, sigma) in global shift order.  One collective: the int64 counts
+        and the float64 shifts (bit-cast to int64) travel in one int64 tensor."""
         if self.world == 1:
-            return local
+            return nus, sig
         import torch
         import torch.distributed as dist
-        t = torch.from_numpy(local)
+        packed = np.concatenate([nus.astype(np.int64), sig.astype(np.float64).view(np.int64)])
+        t = torch.from_numpy(packed)
         if self.device is not None:
             t = t.to(self.device)
-        out = torch.empty(self.world * local.shape[0], dtype=torch.int64, device=t.device)
+        out = torch.empty(self.world * packed.shape[0], dtype=torch.int64, device=t.device)
         dist.all_gather_into_tensor(out, t, group=self.group)
+        g = out.cpu().numpy().reshape(self.world, 2, -1)
         # rank r holds shifts r, r+world, ... ; restore shift order
-        return out.cpu().numpy().reshape(self.world, -1).T.reshape(-1)
+        nu_all = g[:, 0, :].T.reshape(-1).copy()
+        sig_all = g[:, 1, :].copy().view(np.float64).T.reshape(-1).copy()
+        return nu_all, sig_all
 
     def round(self, b: Bracket) -> Bracket:
-        sig_all = self.shifts(b)
-        mine = sig_all[self.rank::self.world].copy()
-        nus = self._allgather(self._local(mine, b.hi - b.lo))
+        sig_plan = self.shifts(b)
+        mine = sig_plan[self.rank::self.world]
+        nus_loc, sig_loc = self._local(mine, b.hi - b.lo)
+        nus, sig_all = self._allgather(nus_loc, sig_loc)
+        # the bracket pairs every count with the shift it was evaluated at (a perturbed
+        # singular shift included), so nu(sigma) = #{lambda < sigma} holds for both ends
         sig_full = np.concatenate([[b.lo], sig_all, [b.hi]])
         nu_full = np.concatenate([[b.nu_lo], nus, [b.nu_hi]])
+        if np.any(np.diff(sig_full) <= 0):
+            raise RuntimeError("perturbed shifts are not increasing")
         if np.any(np.diff(nu_full) < 0):
             raise RuntimeError("nu is not monotone in sigma: inconsistent counts")
         j = int(np.searchsorted(nu_full, self.k, side="left")) - 1     # first pair nu_a < k <= nu_b
@@ -113,3 +127,11 @@ class Multisection:
                 break
             b = self.round(b)
         return b
+
+    def step(self, b: Bracket, initial: Bracket) -> Tuple[Bracket, bool]:
+        """One round of a repeated stage 2 (the benchmark step): returns the new bracket,
+        or `initial` again (restart) once the bracket holds <= m_max eigenvalues."""
+        nb = self.round(b)
+        if nb.count <= self.m_max:
+            return initial, True
+        return nb, False

@@ -41,15 +41,27 @@ def test_single_process_reaches_m_max():
     assert b1.hi - b1.lo == pytest.approx((b0.hi - b0.lo) / 2)
 
 
-def test_singular_shift_is_perturbed():
-    w = _spectrum(200, 1)
+def _with_eig_at(w, x):
+    return np.sort(np.concatenate([w, [x]]))
+
+
+@pytest.mark.parametrize("end", ["hi", "lo"])
+def test_singular_shift_is_perturbed(end):
+    """A singular shift sits on an eigenvalue: the bracket must pair the count with the
+    perturbed shift it was evaluated at (nu(sigma + delta) was paired with sigma)."""
     P = 4
-    b = Bracket(-6.0, 6.0, 0, 200)
-    ms = Multisection(_nu_factory(w), k=50, shifts_per_rank=P)
-    bad = ms.shifts(b)[1]
-    ms2 = Multisection(_nu_factory(w, singular_at=[bad]), k=50, shifts_per_rank=P)
-    nb = ms2.round(b)
-    assert nb.nu_lo < 50 <= nb.nu_hi
+    b = Bracket(-6.0, 6.0, 0, 201)
+    bad = Multisection(None, k=1, shifts_per_rank=P).shifts(b)[1]
+    w = _with_eig_at(_spectrum(200, 1), bad)
+    kb = int(np.searchsorted(w, bad, side="left"))      # w[kb] == bad
+    k = kb + 1 if end == "hi" else kb + 2               # bracket ends (hi) / starts (lo) at the bad shift
+    ms = Multisection(_nu_factory(w, singular_at=[bad]), k=k, shifts_per_rank=P)
+    nb = ms.round(b)
+    assert nb.nu_lo < k <= nb.nu_hi
+    assert np.searchsorted(w, nb.lo, side="left") == nb.nu_lo
+    assert np.searchsorted(w, nb.hi, side="left") == nb.nu_hi
+    moved = nb.hi if end == "hi" else nb.lo
+    assert moved != bad and abs(moved - bad) <= 4e-6 * (b.hi - b.lo)
 
 
 def _free_port():
@@ -70,6 +82,31 @@ def _worker(rank, world, port, k, out):
     b = ms.run(Bracket(-6.0, 6.0, 0, len(w)))
     out[rank] = (b.lo, b.hi, b.nu_lo, b.nu_hi, len(ms.trace))
     dist.destroy_process_group()
+
+
+def _worker_singular(rank, world, port, out):
+    """The singular shift is rank 1's: rank 0 must learn the perturbed shift too."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b = Bracket(-6.0, 6.0, 0, 201)
+    bad = Multisection(None, k=1, shifts_per_rank=2, world=world).shifts(b)[1]   # global shift 1 -> rank 1
+    w = _with_eig_at(_spectrum(200, 1), bad)
+    k = int(np.searchsorted(w, bad, side="left"))
+    ms = Multisection(_nu_factory(w, singular_at=[bad]), k=k, shifts_per_rank=2, rank=rank, world=world)
+    nb = ms.round(b)
+    out[rank] = (nb.lo, nb.hi, nb.nu_lo, nb.nu_hi, int(np.searchsorted(w, nb.hi, side="left")), bad)
+    dist.destroy_process_group()
+
+
+def test_two_ranks_gloo_singular_shift_shared():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_singular, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out[0] == out[1]
+    lo, hi, nlo, nhi, nu_at_hi, bad = out[0]
+    assert nhi == nu_at_hi and hi != bad
 
 
 def test_two_ranks_gloo_agree_with_single():

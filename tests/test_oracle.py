@@ -248,3 +248,54 @@ def test_brute_symbolic_closed_forms():
     # diagonal: every column a root, nzf = n
     c_d, par_d = brute_symbolic(n, np.arange(n + 1, dtype=np.int64), np.arange(n), np.arange(n))
     assert np.sum(c_d) == n and np.all(par_d == -1)
+
+
+# ---------------------------------------------------------------- blocked O-sparse panel
+@pytest.mark.parametrize("f,q,zero_diag,u,seed", [(60, 40, True, 0.01, 0), (60, 40, True, 0.5, 1),
+                                                  (90, 90, True, 0.01, 2), (80, 30, False, 0.3, 3),
+                                                  (120, 70, True, 0.45, 4)])
+def test_blocked_panel_matches_unblocked_front(f, q, zero_diag, u, seed):
+    """The blocked front kernel takes the unblocked loop's decisions: same pivot order,
+    delays, 2x2 count and inertia, and the same contribution block (rounding only)."""
+    from oracle.sparse_mf import _partial_fs_bk, _partial_fs_bk_blocked
+    rng = np.random.default_rng(seed)
+    S = _rand_sym(rng, f, zero_diag)
+    root = q == f
+    F0 = S.copy()
+    r0, o0, e0 = _partial_fs_bk(F0, q, u=u, root=root)
+    for nb in (1, 2, 5, 16, 64):
+        F1 = np.asfortranarray(S.copy())
+        r1, o1, e1 = _partial_fs_bk_blocked(F1, q, u=u, root=root, nb=nb)
+        assert e1 == e0 and np.array_equal(o1, o0)
+        assert (r1.n_neg, r1.n_pos, r1.n_zero, r1.n_2x2, r1.n_delayed) == \
+               (r0.n_neg, r0.n_pos, r0.n_zero, r0.n_2x2, r0.n_delayed)
+        assert np.allclose(F1[e0:, e0:], F0[e0:, e0:], rtol=0, atol=1e-11 * np.max(np.abs(S)))
+    if root:    # a root runs plain BK: its inertia is the matrix's (eigvalsh)
+        w = np.linalg.eigvalsh(S)
+        assert (r0.n_neg, r0.n_pos) == (int(np.sum(w < 0)), int(np.sum(w > 0)))
+
+
+def test_blocked_sparse_oracle_vs_eigh_and_unblocked():
+    # u = 0.5 forces delays; the blocked oracle must agree with eigh (P1) and the unblocked loop
+    p = kepgen.tb_pencil(shape=(5, 5, 6), o=4, seed=12)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    so = oracle.SparseOracle(p)
+    delayed = 0
+    for s in kepgen.uniform_shifts(w[0], w[-1], 8):
+        for u in (0.01, 0.5):
+            r0 = so.inertia(s, u=u)
+            r1 = so.inertia(s, u=u, nb=8)
+            assert r1.n_neg == oracle.nu_eig(A, B, s, eigvals=w)
+            assert (r1.n_neg, r1.n_delayed, r1.n_2x2) == (r0.n_neg, r0.n_delayed, r0.n_2x2)
+            delayed += r1.n_delayed
+    assert delayed > 0
+
+
+def test_blocked_sparse_oracle_twin_mid_size():
+    # n = 6400 with the cutoff-2.2-like pattern (c5 geometry in miniature): blocked O-sparse vs closed form
+    q = kepgen.twin_pencil((8, 10, 20), 4, uA=0.08, uB=0.01, seed=106)
+    w = oracle.twin_eigenvalues(q.meta["twin"])
+    so = oracle.SparseOracle(q)
+    for s in kepgen.uniform_shifts(w[0], w[-1], 5):
+        assert so.inertia(s, nb=32).n_neg == oracle.nu_twin(q.meta["twin"], s, w)
