@@ -6,18 +6,31 @@ Workload (BASELINE.json configs[3], "c4"): the n = 1,500,000 quasi-1D
 tight-binding pencil (10 x 10 x 3750 atoms, 4 orbitals, periodic z, cutoff
 1.8), synthetic and seeded (kepgen).  One STEP is
 one multisection round of stage 2 (Alg. 1' generalised to P = N x S shifts per
-round): every rank factorises S = 16 shifts of the current
-bracket (one LDL^T of A - sigma B each, rows a1-a5 of SURVEY.md §8), the int64
-counts are all-gathered over NCCL and every rank applies the same bracket
-update; a converged bracket (nu_u - nu_l <= m_max = 20) restarts from the
-initial one.  Weak scaling: S shifts per GPU per step.
+round; paper_1710_05134_b200.multisection): every rank
+factorises S = 16 shifts of the current bracket (one LDL^T of A - sigma B each,
+rows a1-a5 of SURVEY.md §8), the int64 counts (and the shifts actually
+evaluated) are all-gathered over NCCL and every rank applies the same bracket
+update; a bracket holding <= m_max = 20 eigenvalues restarts from the initial
+one.  Weak scaling: S shifts per GPU per step.
 
 value = shifts factorised by all ranks / max-over-ranks device time of the K
 timed steps (CUDA events on the library's stream, barrier + synchronize on
 both sides).  e2e = the same through the public C-ABI call with HOST buffers:
 every step uploads A and B values from pinned host memory (kep_set_values)
 and reads the counts back.  The fronts (tens of GB) are far larger than L2,
-so no L2 flush is needed between steps.
+so no L2 flush is needed between steps.  time_to_bracket = one complete
+stage 2 from the initial interval to nu_u - nu_l <= m_max.
+
+--gpus N without torchrun's environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1).
+
+cpu_baseline / --impl reference: the CPU oracle (oracle.sparse_mf, O-sparse,
+as it stands) on C = all host cores, one shift per worker process with one
+BLAS thread (shift-parallel, like multisection), on a bounded sample of the
+workload: the c4 recipe on a 10 x 10 x L periodic sub-wire.  Its measured
+wall time is scaled to full-size c4 shifts by the ratio of the oracle's own
+flop counts (tests/golden/oracle_flops.json, written by
+scripts/oracle_flops.py); the scale and the unscaled numbers are reported.
 """
 from __future__ import annotations
 
@@ -76,7 +89,8 @@ def _clock_summary(lines):
 
 
 def fp64_peak_tflops():
-    """cuBLAS DGEMM 8192^3 best of 5 (the FP64 roofline denominator, measured live)."""
+    """cuBLAS DGEMM 8192^3 best of 5 (the FP64 roofline denominator, measured live:
+    MEASURED_PEAKS.json has no FP64 entry)."""
     import torch
     N = 8192
     a = torch.randn(N, N, dtype=torch.float64, device="cuda")
@@ -97,90 +111,130 @@ def fp64_peak_tflops():
     return 2.0 * N ** 3 / best / 1e12
 
 
-def traffic_per_launch(path=os.path.join(ROOT, "profiles", "r1_schur_traffic.json")):
-    """DRAM bytes (read + write) per k_schur launch, from the committed ncu capture of this
-    bench command (scripts/ncu_traffic.py); None if absent."""
-    try:
-        with open(path) as fh:
-            return json.load(fh)["dram_bytes_per_launch"]
-    except Exception:
-        return None
-
-
-# ----------------------------------------------------------------------------- CPU oracle leg
-def cpu_oracle_sample(cfg: int, seconds_hint: float = 20.0):
-    """Time the oracle (O-sparse, as it stands) on a bounded sample of the workload.
-
-    Sample: the c4 recipe on a 10 x 10 x 150 sub-wire (n = 60,000), one shift,
-    1 BLAS thread; scaled to full-size shifts/s by the oracle's own algorithmic
-    flop count (full c4 / sample).  Returns (shifts_per_s_full, dict)."""
+def workload_config(cfg: int, shape, world: int, S: int) -> dict:
+    """The `config` object of the JSON line: the workload only, identical in both arms."""
     import kepgen
-    import oracle
-    from oracle.sparse_mf import SparseOracle
+    kw = dict(kepgen.CONFIGS[cfg])
+    shp = tuple(shape) if shape else kw["shape"]
+    n = int(np.prod(shp)) * kw["o"]
+    return {"workload": f"c{cfg}" + (f"-{'x'.join(map(str, shp))}" if shape else ""),
+            "lattice": "x".join(map(str, shp)), "orbitals": kw["o"], "cutoff": kw["cutoff"],
+            "periodic": list(kw["periodic"]), "seed": kw["seed"], "n": n,
+            "shifts_per_gpu_per_step": S, "shifts_per_step": S * world,
+            "l2": "inputs larger than L2 (fronts ~GBs per shift); no flush"}
+
+
+# ----------------------------------------------------------------------------- CPU oracle (baseline / reference arm)
+_SAMPLE = None
+
+
+def _oracle_worker_init():
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     try:
         from threadpoolctl import threadpool_limits
-    except Exception:                                  # pragma: no cover
-        threadpool_limits = None
-    base = dict(kepgen.CONFIGS[cfg])
-    full_shape = base["shape"]
-    sample_shape = (full_shape[0], full_shape[1], 150) if cfg == 4 else tuple(max(4, s // 3) for s in full_shape)
-    base["shape"] = sample_shape
-    p = kepgen.tb_pencil(**base)
-    so = SparseOracle(p)
-    lo, hi = kepgen.spectral_bounds(p)
-    sig = 0.5 * (lo + hi)
+        threadpool_limits(1)
+    except Exception:                                    # pragma: no cover
+        pass
 
-    def flops_of(orc):
-        piv, fs = orc.front_sizes()
-        tot = 0.0
-        for pp, ff in zip(piv, fs):
-            c = ff - pp
-            m = np.arange(c, ff, dtype=np.float64)
-            tot += float(np.sum(m * m + 2 * m))
-        return tot
 
-    f_sample = flops_of(so)
-    t0 = time.time()
-    if threadpool_limits is not None:
-        with threadpool_limits(1):
-            r = so.inertia(sig)
-    else:
-        r = so.inertia(sig)
-    dt = time.time() - t0
-    # full-size oracle flops: the wire is uniform along z, so the oracle's
-    # symbolic on the full pattern is replaced by the exact length ratio only
-    # when the full symbolic would be too slow; here we compute it.
-    pf = kepgen.tb_pencil(**dict(kepgen.CONFIGS[cfg])) if cfg != 4 else None
-    if pf is not None:
-        f_full = flops_of(SparseOracle(pf))
-    else:
-        f_full = f_sample * (full_shape[2] / sample_shape[2])
-    scale = f_full / f_sample
-    return 1.0 / (dt * scale), dict(sample=f"c{cfg} recipe on a {'x'.join(map(str, sample_shape))} lattice "
-                                          f"(n={p.n}), 1 shift, 1 BLAS thread, scaled x{scale:.2f} by oracle flops",
-                                   seconds=dt, nu=int(r.n_neg), oracle_flops_sample=f_sample, scale=scale)
+def _oracle_worker(sigma):
+    t = time.time()
+    r = _SAMPLE.inertia(float(sigma))
+    return time.time() - t, int(r.n_neg)
+
+
+class OracleSample:
+    """The oracle as it stands on a bounded sample of the workload, C worker processes."""
+
+    def __init__(self, cfg: int, length: int):
+        import kepgen
+        from oracle.sparse_mf import SparseOracle
+        global _SAMPLE
+        if cfg != 4:
+            raise ValueError("the CPU sample is defined for the c4 workload")
+        base = kepgen.CONFIGS[cfg]["shape"]
+        self.shape = (base[0], base[1], length)
+        p = kepgen.config(cfg, shape=self.shape)
+        self.n = p.n
+        _SAMPLE = SparseOracle(p)
+        lo, hi = kepgen.spectral_bounds(p)
+        self.lo, self.hi = lo, hi
+        fl = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_flops.json")))[f"c{cfg}"]
+        self.scale = fl["full"] / fl["x".join(map(str, self.shape))]     # sample shifts per full-size shift
+        self.cores = len(os.sched_getaffinity(0))
+        from multiprocessing import get_context
+        self.pool = get_context("fork").Pool(self.cores, initializer=_oracle_worker_init)
+
+    def step(self, i0: int = 0):
+        """One shift per core, all in parallel; returns (wall s, per-shift seconds)."""
+        from kepgen import uniform_shifts
+        sig = uniform_shifts(self.lo, self.hi, self.cores + 1)[:self.cores]
+        sig = np.roll(sig, i0)
+        t = time.time()
+        res = self.pool.map(_oracle_worker, sig, chunksize=1)
+        return time.time() - t, [r[0] for r in res]
+
+    def describe(self):
+        return (f"c4 recipe on a {'x'.join(map(str, self.shape))} periodic sub-wire (n={self.n}), one shift per "
+                f"core on {self.cores} cores in parallel, 1 BLAS thread each; wall time scaled to full-size "
+                f"c4 shifts by the oracle's own flop ratio x{self.scale:.2f} (tests/golden/oracle_flops.json)")
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the oracle timed as it stands, on this run's config (rank 0 only)."""
     if rank != 0:
         return 0
     K, W = args.steps, args.warmup
-    times = []
-    info = None
+    smp = OracleSample(args.config, args.ref_length)
+    walls, per = [], []
     for i in range(W + K):
-        v, info = cpu_oracle_sample(args.config)
+        wall, ts = smp.step(i)
         if i >= W:
-            times.append(1.0 / v)
-    t = float(np.mean(times))
-    val = 1.0 / t
+            walls.append(wall)
+            per += ts
+    smp.close()
+    wall = float(np.mean(walls))
+    shift_eq = smp.cores / smp.scale                  # full-size c4 shift equivalents per step
+    val = shift_eq / wall
+    cfgd = workload_config(args.config, None, args.gpus, args.shifts_per_gpu)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "shifts/s", "n_gpus": args.gpus,
-            "steps": K, "warmup": W, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"c{args.config}", "shifts_per_step": 1},
-            "cpu_baseline": {"value": val, "unit": "shifts/s", "cores": 1, "kind": "oracle", "sample": info["sample"]},
+            "steps": K, "warmup": W, "ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
+            "cpu_baseline": {"value": val, "unit": "shifts/s", "cores": smp.cores, "kind": "oracle",
+                             "sample": smp.describe(),
+                             "sample_shifts_per_step": smp.cores,
+                             "full_shift_equivalents_per_step": shift_eq,
+                             "sample_seconds_per_shift_mean": float(np.mean(per)),
+                             "extrapolated_seconds_per_full_shift_1core": float(np.mean(per)) * smp.scale},
             "e2e": {"value": val, "unit": "shifts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baseline_leg(cfg, length):
+    smp = OracleSample(cfg, length)
+    wall, ts = smp.step(0)
+    smp.close()
+    v = smp.cores / smp.scale / wall
+    return {"value": v, "unit": "shifts/s", "cores": smp.cores, "kind": "oracle", "sample": smp.describe(),
+            "sample_wall_s": wall, "sample_seconds_per_shift_mean": float(np.mean(ts)),
+            "extrapolated_seconds_per_full_shift_1core": float(np.mean(ts)) * smp.scale}
+
+
+# ----------------------------------------------------------------------------- multi-rank launch
+def _relaunch_torchrun(n):
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -195,8 +249,12 @@ def main():
     ap.add_argument("--shape", default=None, help="override lattice, e.g. 10x10x400 (development only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-length", type=int, default=150, help="sub-wire length of the cpu_baseline sample")
+    ap.add_argument("--ref-length", type=int, default=100, help="sub-wire length of the reference-arm sample")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return _relaunch_torchrun(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -207,17 +265,19 @@ def main():
     import torch.distributed as dist
     import kepgen
     from paper_1710_05134_b200 import Kep
+    from paper_1710_05134_b200.multisection import Bracket, Multisection
 
     torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.init_process_group("nccl", device_id=dev)
 
     def log(*a):
         if rank == 0:
             print(*a, file=sys.stderr, flush=True)
 
-    # ---- synthetic input: generated on rank 0, broadcast (replicated pencil, PAPER path shards by shift)
+    # ---- synthetic input: generated on rank 0, broadcast (replicated pencil; the path shards by shift)
     t0 = time.time()
     shape = tuple(int(x) for x in args.shape.split("x")) if args.shape else None
     meta = [None]
@@ -232,7 +292,6 @@ def main():
     if rank == 0:
         colptr, rowidx, a, b = p.colptr, p.rowidx, p.a, p.b
     if world > 1:
-        dev = torch.device("cuda", local_rank)
         if rank == 0:
             tc = torch.from_numpy(colptr).to(dev); tr = torch.from_numpy(rowidx).to(dev)
             ta = torch.from_numpy(a).to(dev); tb = torch.from_numpy(b).to(dev)
@@ -244,7 +303,7 @@ def main():
         colptr, rowidx, a, b = (t.cpu().numpy() for t in (tc, tr, ta, tb))
         del tc, tr, ta, tb
     t_gen = time.time() - t0
-    log(f"[bench] input {meta['name']} n={n} nnz_lower={nnz} ready in {t_gen:.1f}s")
+    log(f"[bench] input {meta['name']} n={n} nnz_lower={nnz} ready in {t_gen:.1f}s world={world}")
 
     S = args.shifts_per_gpu
     t0 = time.time()
@@ -257,42 +316,26 @@ def main():
     peak = fp64_peak_tflops() if rank == 0 else 0.0
 
     P = world * S
-    kk = meta["k"]
-    lo0, hi0 = meta["lo"], meta["hi"]
-    state = dict(lo=lo0, hi=hi0, nlo=0, nhi=n, rounds=0, restarts=0, redo=0, delayed=0, evals=0)
+    initial = Bracket(meta["lo"], meta["hi"], 0, n)
+    stats = dict(redo=0, delayed=0, evals=0, restarts=0, rounds=0)
+
+    def nu_many(sig):
+        nus, st, infos = k.inertia_many(sig, with_info=True)
+        stats["redo"] += sum(i.n_redo for i in infos)
+        stats["delayed"] += sum(i.n_delayed for i in infos)
+        stats["evals"] += len(infos)
+        return nus, st
+
+    ms = Multisection(nu_many, k=meta["k"], shifts_per_rank=S, m_max=M_MAX, rank=rank, world=world,
+                      device=dev if world > 1 else None)
+    state = {"b": initial}
 
     def one_round(set_vals=None):
-        """One multisection round: P interior shifts of [lo, hi), this rank takes i = rank mod world."""
         if set_vals is not None:
             set_vals()
-        lo, hi = state["lo"], state["hi"]
-        sig_all = lo + (np.arange(P) + 1.0) * (hi - lo) / (P + 1)
-        mine = sig_all[rank::world]
-        nus, st, infos = k.inertia_many(mine, with_info=True)
-        state["redo"] += sum(i.n_redo for i in infos)
-        state["delayed"] += sum(i.n_delayed for i in infos)
-        state["evals"] += len(infos)
-        nus = np.where(st == 0, nus, -1).astype(np.int64)
-        if world > 1:
-            t = torch.from_numpy(nus).cuda()
-            out = torch.empty(world * len(nus), dtype=torch.int64, device=t.device)
-            dist.all_gather_into_tensor(out, t)
-            allv = out.cpu().numpy().reshape(world, -1).T.reshape(-1)      # back to shift order
-        else:
-            allv = nus
-        # bracket update (SURVEY.md §8(c) reading 12): first pair with nu_a < k <= nu_b
-        nus_full = np.concatenate([[state["nlo"]], allv, [state["nhi"]]])
-        sig_full = np.concatenate([[lo], sig_all, [hi]])
-        ok = np.all(allv >= 0)
-        if ok:
-            for j in range(len(sig_full) - 1):
-                if nus_full[j] < kk <= nus_full[j + 1]:
-                    state.update(lo=sig_full[j], hi=sig_full[j + 1], nlo=int(nus_full[j]), nhi=int(nus_full[j + 1]))
-                    break
-        state["rounds"] += 1
-        if state["nhi"] - state["nlo"] <= M_MAX or not ok:
-            state.update(lo=lo0, hi=hi0, nlo=0, nhi=n)
-            state["restarts"] += 1
+        state["b"], restarted = ms.step(state["b"], initial)
+        stats["rounds"] += 1
+        stats["restarts"] += int(restarted)
 
     for _ in range(args.warmup):
         one_round()
@@ -319,7 +362,7 @@ def main():
     stop.set()
     dev_s = ev0.elapsed_time(ev1) / 1e3
     prof = k.profile()
-    t_max = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+    t_max = torch.tensor([dev_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     t_max = float(t_max.item())
@@ -342,45 +385,63 @@ def main():
             one_round(set_vals=lambda: k.set_values(pa, pb))
         e1.record()
         torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+        te = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": shifts_total / float(te.item()), "unit": "shifts/s",
                "h2d_bytes_per_step": int(2 * nnz * 8 + S * 8), "d2h_bytes_per_step": int(S * 8)}
 
+    # ---- time to bracket: one complete stage 2 from the initial interval
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    b2b0, b2b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b2b0.record()
+    ms.trace.clear()
+    fin = ms.run(initial)
+    b2b1.record()
+    torch.cuda.synchronize()
+    tb = torch.tensor([b2b0.elapsed_time(b2b1) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+    to_bracket = {"seconds": float(tb.item()), "rounds": len(ms.trace), "shifts_per_round": P,
+                  "k": meta["k"], "bracket": [fin.lo, fin.hi, fin.nu_lo, fin.nu_hi],
+                  "table5_analogue": [{"interval": list(r.bracket[:2]), "index_range": list(r.bracket[2:]),
+                                       "m": r.bracket[3] - r.bracket[2]} for r in ms.trace]}
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, info = cpu_oracle_sample(args.config)
-        cpu = {"value": v, "unit": "shifts/s", "cores": 1, "kind": "oracle", "sample": info["sample"]}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == 4 and not args.shape:
+        cpu = cpu_baseline_leg(args.config, args.cpu_length)
 
     if rank == 0:
-        ms = prof["ms"]
-        dom = max(ms, key=lambda x: ms[x])
-        sch_t = ms["schur"] / 1e3
+        msd = prof["ms"]
+        dom = max(msd, key=lambda x: msd[x])
+        sch_t = msd["schur"] / 1e3
         roof = {"bound": "tensor", "kernel": "k_schur (a4, DMMA f64)",
                 "achieved": (prof["schur_flops"] / sch_t / 1e12) if sch_t > 0 else None,
                 "peak": peak, "unit": "TFLOP/s",
                 "frac": (prof["schur_flops"] / sch_t / 1e12 / peak) if sch_t > 0 and peak > 0 else None,
-                "traffic": traffic_per_launch(),
+                "traffic": None,
+                "traffic_note": "not measured by this run; ncu DRAM bytes of k_schur are in profiles/",
                 "peak_source": "cuBLAS DGEMM 8192^3 measured live in bench.py (MEASURED_PEAKS.json has no FP64 entry)",
-                "kernel_ms": ms, "kernel_launches": prof["launches"], "dominant_by_time": dom,
+                "kernel_ms": msd, "kernel_launches": prof["launches"], "dominant_by_time": dom,
                 "schur_flops_alg": prof["schur_flops"]}
         launches = int(sum(prof["launches"].values()) + prof["other_launches"])
         fac_tflops = ana["flops"] * shifts_total / t_max / world / 1e12
         line = {"metric": METRIC, "value": value, "unit": "shifts/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"c{args.config}" + (f"-{args.shape}" if args.shape else ""), "n": n,
-                           "nnz_lower": nnz, "shifts_per_gpu_per_step": S, "shifts_per_step": P,
-                           "l2": "inputs larger than L2 (fronts ~GBs); no flush",
-                           "flops_per_shift_alg": ana["flops"], "factor_tflops_per_gpu": fac_tflops,
-                           "factor_tflops_frac_of_fp64_peak": fac_tflops / peak if peak else None,
-                           "fronts": ana["n_fronts"], "levels": ana["n_levels"], "max_front": ana["max_front"],
-                           "multisection_rounds": state["rounds"], "restarts": state["restarts"],
-                           "delayed_pivots_per_shift": state["delayed"] / max(state["evals"], 1),
-                           "fast_path_reruns_per_shift": state["redo"] / max(state["evals"], 1)},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": _clock_summary(clocks), "wall_s": wall,
+                "config": workload_config(args.config, shape, world, S),
+                "stats": {"nnz_lower": nnz, "flops_per_shift_alg": ana["flops"],
+                          "factor_tflops_per_gpu": fac_tflops,
+                          "factor_tflops_frac_of_fp64_peak": fac_tflops / peak if peak else None,
+                          "fronts": ana["n_fronts"], "levels": ana["n_levels"], "max_front": ana["max_front"],
+                          "arena_gb_per_shift": ana["arena_bytes"] / 1e9, "batch": ana["batch"],
+                          "multisection_rounds": stats["rounds"], "restarts": stats["restarts"],
+                          "delayed_pivots_per_shift": stats["delayed"] / max(stats["evals"], 1),
+                          "fast_path_reruns_per_shift": stats["redo"] / max(stats["evals"], 1)},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "time_to_bracket": to_bracket,
+                "gpu_launches": launches, "clocks": _clock_summary(clocks), "wall_s": wall,
                 "setup_s": {"generate": t_gen, "analyze": t_an}}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -202,6 +202,18 @@ KEP_API kep_status kep_factor(kep_ctx* ctx, double sigma, kep_factorization** ou
  * B-solves of stage 1's generalized Lanczos). */
 KEP_API kep_status kep_factor_pencil(kep_ctx* ctx, double alpha, double sigma, kep_factorization** out);
 
+/* Front-local bound of the factor residual at sigma (SURVEY.md §8(c) item 13,
+ * the P8 pin of the BASELINE north_star at sizes where the dense residual
+ * cannot be formed).  Factorises A - sigma B exactly as kep_factor does and,
+ * per front s, evaluates E_s = P_s F_s P_s^T - L_s D_s L_s^T - (0 (+) T_s)
+ * (F_s the assembled front, T_s the trailing block its parent extend-adds);
+ * these telescope over the assembly tree, so
+ *     || P (A - sigma B) P^T - L D L^T ||_F <= *bound = sum_s ||E_s||_F.
+ * *max_front (nullable) = max_s ||E_s||_F.  Diagnostics only: needs one extra
+ * front arena of device memory; no factor is kept.  Errors: as kep_factor
+ * (KEP_ESINGULAR is not raised: the bound is reported at any shift). */
+KEP_API kep_status kep_factor_residual(kep_ctx* ctx, double sigma, double* bound, double* max_front);
+
 /* Factor statistics (shift, nu, inertia, size of L). */
 KEP_API kep_status kep_factor_info(const kep_factorization* f, kep_factor_stats* out);
 

@@ -97,6 +97,11 @@ struct kep_ctx {
     std::vector<int> level_qmax;                // per level: max p + slack over its fast fronts
     std::vector<double> item_flops;             // per level: algorithmic a4 flops of its fast fronts
     std::vector<kep_factorization*> factors;    // live factors (released by kep_destroy)
+    // kep_factor_residual: captured fronts, per-front sum of squares, residual tiles per level
+    double* d_f0 = nullptr;
+    double* d_resid = nullptr;
+    int4* d_ritems = nullptr;
+    std::vector<int64_t> ritem_off, ritem_cnt;
     // profiling
     kep_profile prof;
     std::vector<cudaEvent_t> ev_pool;
@@ -612,7 +617,7 @@ kep_status prepare_store(kep_ctx* c, kep_factorization* k) {
 // One batch of `m` shifts through every level.  Fills c->h_stats[0..m).
 // keep != NULL (m == 1): the factors are copied into keep's store level by level.
 kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization* keep = nullptr,
-                     double alpha = 1.0) {
+                     double alpha = 1.0, bool resid = false) {
     for (int attempt = 0; attempt < 8; ++attempt) {
         if (m > c->batch_cap) return fail(c, KEP_EINVAL, "internal: batch larger than capacity");
         if (keep) {
@@ -652,6 +657,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             if (c->asm_red[L]) kep::launch_assemble_red(P, c->d_level_fronts + b, nfl, m, c->stream);
             else kep::launch_assemble(P, c->d_aitems + c->aitem_off[L], (int)c->aitem_cnt[L], m, false, c->stream);
             mark(KEP_K_ASSEMBLE, false);
+            if (resid) kep::launch_capture(P, c->d_level_fronts + b, nfl, c->d_f0, c->stream);
             c->prof.launches[KEP_K_ASSEMBLE]++;
             if (c->fast_cnt[L]) {
                 const int32_t* fl = c->d_lists + c->fast_off[L];
@@ -767,6 +773,9 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 c->prof.launches[KEP_K_SCHUR] += (c->item_cnt[L] ? 1 : 0) + (c->small_cnt[L] ? 1 : 0);
                 c->prof.schur_flops += c->item_flops[L] * m;
             }
+            if (resid)
+                kep::launch_resid(P, keep->plan(), c->d_ritems + c->ritem_off[L], (int)c->ritem_cnt[L], c->d_f0,
+                                  c->d_resid, c->stream);
         }
         KEP_CUDA(c, cudaGetLastError());
         KEP_CUDA(c, cudaMemcpyAsync(c->h_stats.data(), c->d_stats, sizeof(ShiftStat) * m, cudaMemcpyDeviceToHost, c->stream));
@@ -1014,6 +1023,96 @@ kep_status kep_factor_pencil(kep_ctx* c, double alpha, double sigma, kep_factori
     c->factors.push_back(k);
     *out = k;
     return KEP_OK;
+}
+
+kep_status kep_factor_residual(kep_ctx* c, double sigma, double* bound, double* max_front) {
+    if (!c || !bound) return fail(c, KEP_EINVAL, "null argument");
+    if (!c->have_device) return fail(c, KEP_ENODEVICE, "no CUDA device");
+    if (!c->values_set) return fail(c, KEP_EINVAL, "kep_set_values must precede kep_factor_residual");
+    KEP_CUDA(c, cudaSetDevice(c->device));
+    const Symbolic& S = c->sym;
+    const int nl = (int)S.level_ptr.size() - 1;
+    kep_factorization* k = new (std::nothrow) kep_factorization();
+    if (!k) return fail(c, KEP_ENOMEM, "host allocation failed");
+    k->ctx = c;
+    k->sigma = sigma;
+    kep_status st = KEP_OK;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        // residual tiles (front, I, J) of every level, by capacity (fronts may grow by delays)
+        std::vector<int4> it;
+        c->ritem_off.assign(nl, 0);
+        c->ritem_cnt.assign(nl, 0);
+        const int RB = kep::resid_tile();
+        for (int L = 0; L < nl; ++L) {
+            c->ritem_off[L] = (int64_t)it.size();
+            for (int x = S.level_ptr[L]; x < S.level_ptr[L + 1]; ++x) {
+                const int s = S.level_fronts[x];
+                const int nt = (S.capacity[s] + RB - 1) / RB;
+                for (int I = 0; I < nt; ++I)
+                    for (int J = 0; J <= I; ++J) it.push_back(make_int4(s, I, J, 0));
+            }
+            c->ritem_cnt[L] = (int64_t)it.size() - c->ritem_off[L];
+        }
+        cudaFree(c->d_ritems); c->d_ritems = nullptr;
+        cudaFree(c->d_f0); c->d_f0 = nullptr;
+        cudaFree(c->d_resid); c->d_resid = nullptr;
+        KEP_CUDA(c, upload(&c->d_ritems, it));
+        KEP_CUDA(c, cudaMalloc(&c->d_f0, std::max<int64_t>(S.arena_doubles, 1) * sizeof(double)));
+        KEP_CUDA(c, cudaMalloc(&c->d_resid, std::max<int64_t>(S.nf, 1) * 4 * sizeof(double)));
+        KEP_CUDA(c, cudaMemsetAsync(c->d_resid, 0, std::max<int64_t>(S.nf, 1) * 4 * sizeof(double), c->stream));
+        const int32_t slack0 = S.slack;
+        st = run_batch(c, 1, &sigma, k, 1.0, true);
+        if (st != KEP_OK || S.slack == slack0) break;         // a replan changes capacities: redo the tiles
+    }
+    if (st == KEP_OK) {
+        std::vector<double> r(std::max<int64_t>(S.nf, 1) * 4);
+        KEP_CUDA(c, cudaMemcpy(r.data(), c->d_resid, sizeof(double) * r.size(), cudaMemcpyDeviceToHost));
+        double sum = 0.0, mx = 0.0;
+        const bool dbg = getenv("KEP_DEBUG_RESID") != nullptr;
+        std::vector<int4> hdr;
+        if (dbg) {
+            hdr.resize(S.nf);
+            KEP_CUDA(c, cudaMemcpy(hdr.data(), k->hdr, sizeof(int4) * S.nf, cudaMemcpyDeviceToHost));
+        }
+        if (const char* dump = getenv("KEP_DEBUG_DUMP")) {      // one front: F0, arena, perm, store
+            const int64_t s2 = atoll(dump);
+            const int4 h = hdr[s2];
+            const int f = h.y, ld = kep::ldpad(f), q = h.z, e = h.x;
+            std::vector<double> f0((size_t)f * ld), fa((size_t)f * ld), pan((size_t)f * e);
+            std::vector<double> aux((size_t)(S.capacity[s2] - S.ncb[s2]) * kep::AUX_W);
+            std::vector<int64_t> aoff(S.nf);
+            cudaMemcpy(aoff.data(), c->d_aux_off, sizeof(int64_t) * S.nf, cudaMemcpyDeviceToHost);
+            cudaMemcpy(f0.data(), c->d_f0 + S.arena_off[s2], f0.size() * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(fa.data(), c->d_arena + S.arena_off[s2], fa.size() * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(pan.data(), k->panel + k->h_poff[s2], pan.size() * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(aux.data(), c->d_aux + aoff[s2] * kep::AUX_W, aux.size() * 8, cudaMemcpyDeviceToHost);
+            std::vector<int32_t> lab(f);
+            cudaMemcpy(lab.data(), k->lab + k->h_loff[s2], f * 4, cudaMemcpyDeviceToHost);
+            FILE* fp = fopen("gpurun_out/dump_front.bin", "wb");
+            int hd[6] = {e, f, q, h.w, ld, S.capacity[s2] - S.ncb[s2]};
+            fwrite(hd, 4, 6, fp);
+            fwrite(f0.data(), 8, f0.size(), fp); fwrite(fa.data(), 8, fa.size(), fp); fwrite(pan.data(), 8, pan.size(), fp);
+            fwrite(aux.data(), 8, aux.size(), fp); fwrite(lab.data(), 4, lab.size(), fp);
+            fclose(fp);
+        }
+        for (int64_t s2 = 0; s2 < S.nf; ++s2) {
+            const double v = std::sqrt(std::max(r[4 * s2], 0.0));
+            sum += v;
+            mx = std::max(mx, v);
+            if (dbg && v > 1e-12)
+                fprintf(stderr, "[resid] front %lld e=%d f=%d q=%d flag=%d p=%d c=%d |E|=%.3e FSxE=%.3e CBxE=%.3e TT=%.3e\n",
+                        (long long)s2, hdr[s2].x, hdr[s2].y, hdr[s2].z, hdr[s2].w, (int)S.npiv[s2], (int)S.ncb[s2], v,
+                        std::sqrt(r[4 * s2 + 1]), std::sqrt(r[4 * s2 + 2]), std::sqrt(r[4 * s2 + 3]));
+        }
+        *bound = sum;
+        if (max_front) *max_front = mx;
+    }
+    cudaFree(c->d_ritems); c->d_ritems = nullptr;
+    cudaFree(c->d_f0); c->d_f0 = nullptr;
+    cudaFree(c->d_resid); c->d_resid = nullptr;
+    free_store(k);
+    delete k;
+    return st;
 }
 
 kep_status kep_factor_info(const kep_factorization* k, kep_factor_stats* out) {
@@ -1545,7 +1644,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
                         c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1], c->d_rr_l[2], c->d_rr_u, c->d_rr_a, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
-                        c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small};
+                        c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small, c->d_f0, c->d_resid, c->d_ritems};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -184,6 +184,11 @@ void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, in
 bool schur_small_ok(int c, int qcap);     // front handled by k_schur_small
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,
                         bool only_flagged = false);
+// kernels_resid.cu: front-local factor residual (kep_factor_residual)
+int resid_tile();
+void launch_capture(const DevPlan& P, const int32_t* fronts, int nfronts, double* F0, cudaStream_t st);
+void launch_resid(const DevPlan& P, const StorePlan& T, const int4* items, int nitems, const double* F0, double* out,
+                  cudaStream_t st);
 void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st);
 void launch_reset_stats(ShiftStat* st, int batch, cudaStream_t s);
 

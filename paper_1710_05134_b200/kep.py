@@ -121,6 +121,8 @@ def lib():
         L.kep_solve_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.kep_factor_export.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_int64),
                                         P(C.c_int32), P(C.c_double)]
+        L.kep_factor_residual.argtypes = [C.c_void_p, C.c_double, P(C.c_double), P(C.c_double)]
+        L.kep_factor_residual.restype = C.c_int
         L.kep_factor_destroy.argtypes = [C.c_void_p]
         L.kep_factor_destroy.restype = None
         for f in ("kep_factor", "kep_factor_info", "kep_solve", "kep_solve_dev", "kep_factor_export"):
@@ -269,6 +271,13 @@ class Kep:
         h = C.c_void_p()
         self._check(lib().kep_factor_pencil(self._h, float(alpha), float(sigma), C.byref(h)))
         return Factor(self, h)
+
+    def factor_residual(self, sigma: float):
+        """kep_factor_residual: (sum_s ||E_s||_F, max_s ||E_s||_F), the front-local bound of
+        ||P (A - sigma B) P^T - L D L^T||_F."""
+        bound, mx = C.c_double(np.nan), C.c_double(np.nan)
+        self._check(lib().kep_factor_residual(self._h, float(sigma), C.byref(bound), C.byref(mx)))
+        return bound.value, mx.value
 
     def kth_eigenpair(self, k: int, m_max=20, tau_res=1e-10, tau_diff=1e-10, max_lanczos=64, max_bisect=128,
                       max_si=500, shifts_per_round=1, seed=1, v0_stage1=None, v0_stage3=None, want_x=True,

@@ -1,4 +1,4 @@
-"""Write tests/golden/c{2,4}_nu.json: oracle nu at fixed shifts of the full-size
+"""Write tests/golden/c{2,3,4,5}_nu.json: oracle nu at fixed shifts of the full-size
 configs, for the GPU parity tests at BASELINE sizes.
 
 Calls only ``oracle/`` (O-sparse multifrontal) and the seeded generator
@@ -22,10 +22,11 @@ sys.path.insert(0, ROOT)
 
 _P = None
 _SO = None
+_NB = 0
 
 
-def _init(cfg):
-    global _P, _SO
+def _init(cfg, nb):
+    global _P, _SO, _NB
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from threadpoolctl import threadpool_limits
     threadpool_limits(1)
@@ -33,11 +34,12 @@ def _init(cfg):
     from oracle.sparse_mf import SparseOracle
     _P = kepgen.config(cfg)
     _SO = SparseOracle(_P)
+    _NB = nb
 
 
 def _nu(sigma):
     t = time.time()
-    r = _SO.inertia(sigma)
+    r = _SO.inertia(sigma, nb=_NB)
     return sigma, int(r.n_neg), int(r.n_delayed), bool(r.singular), time.time() - t
 
 
@@ -47,6 +49,8 @@ def main():
     ap.add_argument("--shifts", type=int, default=8)
     ap.add_argument("--procs", type=int, default=8)
     ap.add_argument("--reuse", default=None)
+    ap.add_argument("--nb", type=int, default=None,
+                    help="O-sparse FS panel width (0 = unblocked loop); default 64 for c3 and c5, else 0")
     a = ap.parse_args()
     import numpy as np
     import kepgen
@@ -62,7 +66,8 @@ def main():
         todo = []
         for s in sig:
             todo += [s - d] + ([] if float(s) in old else [s]) + [s + d]
-        with get_context("fork").Pool(a.procs, initializer=_init, initargs=(cfg,)) as pool:
+        nb = a.nb if a.nb is not None else (64 if cfg in (3, 5) else 0)
+        with get_context("fork").Pool(a.procs, initializer=_init, initargs=(cfg, nb)) as pool:
             res = pool.map(_nu, todo)
         out = []
         it = iter(res)
@@ -74,7 +79,7 @@ def main():
             out.append(dict(sigma=float(s), nu=n0, certified=bool(nm == n0 == npl and not (sm or s0 or sp)),
                             oracle_delayed=dl, oracle_seconds=t0))
         doc = {"_source": f"scripts/make_goldens.py: oracle.sparse_mf (O-sparse) on kepgen.config({cfg}) "
-                          f"seed {kepgen.CONFIGS[cfg]['seed']}; certification nu(s-d)==nu(s)==nu(s+d), d={d:.3e}",
+                          f"seed {kepgen.CONFIGS[cfg]['seed']}, FS panel nb={nb}; certification nu(s-d)==nu(s)==nu(s+d), d={d:.3e}",
                "config": cfg, "n": p.n, "nnz_lower": p.nnz, "lo": lo, "hi": hi, "shifts": out}
         path = os.path.join(ROOT, "tests", "golden", f"c{cfg}_nu.json")
         json.dump(doc, open(path, "w"), indent=1)

@@ -121,3 +121,48 @@ def test_factor_c2_probe_residual_and_solve():
     # the factor's inertia agrees with the inertia path at the same shift
     st, nu, _ = k.inertia(sig)
     assert fac.info()["nu"] == nu == _d_inertia(d, ds)
+
+
+# ---------------------------------------------------------------- front-local residual bound
+def _norm_s(p, sig):
+    v = p.a - sig * p.b
+    col = np.repeat(np.arange(p.n), np.diff(p.colptr))
+    diag = p.rowidx == col
+    return float(np.sqrt(np.sum(v[diag] ** 2) + 2.0 * np.sum(v[~diag] ** 2)))
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("u", [0.01, 0.5])
+def test_residual_bound_dominates_exact_c1(u, variant):
+    """sum_s ||E_s||_F >= ||P S P^T - L D L^T||_F (telescoping identity), both <= 1e-10 ||S||_F;
+    the bound is not vacuous: within a small factor of the exact residual's order."""
+    p = kepgen.config(1)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    k = Kep.from_pencil(p, pivot_u=u, kernel_variant=variant)
+    k.set_values(p.a, p.b)
+    for sig in kepgen.uniform_shifts(w[0], w[-1], 4):
+        S = A - sig * B
+        perm, L, D = _dense_ldlt(k.factor(sig).export(), p.n)
+        exact = np.linalg.norm(S[np.ix_(perm, perm)] - L @ D @ L.T)
+        bound, mx = k.factor_residual(sig)
+        ns = np.linalg.norm(S)
+        assert abs(ns - _norm_s(p, sig)) <= 1e-12 * ns
+        assert bound >= exact * (1 - 1e-6) and mx <= bound
+        assert 0.0 < bound <= 1e-10 * ns, (bound / ns, exact / ns)
+
+
+@pytest.mark.parametrize("cfg,nshift", [(2, 3), (3, 2), (4, 2), (5, 1)])
+def test_residual_bound_full_size(cfg, nshift):
+    """P8 at the BASELINE sizes: front-local bound of the factor residual <= 1e-10 ||A - sigma B||_F
+    (c3-c5 exercise the global-scratch pivot blocks, the k_l21<2> explicit-inverse in-block solve (R22)
+    and the multi-tile k_fsu updates)."""
+    p = kepgen.config(cfg)
+    lo, hi = kepgen.spectral_bounds(p)
+    k = Kep.from_pencil(p, max_batch=1)
+    k.set_values(p.a, p.b)
+    for sig in lo + (hi - lo) * np.array([0.31, 0.62, 0.83])[:nshift]:
+        bound, mx = k.factor_residual(sig)
+        rel = bound / _norm_s(p, sig)
+        print(f"c{cfg} sigma={sig:.6f} bound/||S||_F={rel:.3e} max front {mx / _norm_s(p, sig):.3e}")
+        assert 0.0 < rel <= 1e-10, rel

@@ -150,7 +150,7 @@ def test_metamorphic_on_gpu():
     assert np.array_equal(shifted, base) and np.array_equal(neg, p.n - base) and np.array_equal(scl, base)
 
 
-@pytest.mark.parametrize("cfg", [2, 3, 4])
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
 def test_full_size_goldens(cfg):
     """BASELINE full sizes: nu at the certified shifts stored by scripts/make_goldens.py (oracle only)."""
     path = os.path.join(GOLD, f"c{cfg}_nu.json")
