@@ -54,12 +54,14 @@ typedef enum {
     KEP_EPATTERN = 2,     /* values do not match the analysed pattern */
     KEP_ESINGULAR = 3,    /* some |pivot| <= tau_sing * max|A - sigma B|: sigma is
                              (numerically) an eigenvalue; perturb sigma and retry */
-    KEP_ENOTSPD = 4,      /* reserved: B failed an all-positive-pivot check */
+    KEP_ENOTSPD = 4,      /* B failed an all-positive-pivot check (kep_kth_eigenpair) */
     KEP_ENOMEM = 5,       /* host or device allocation failed */
     KEP_ECUDA = 6,        /* a CUDA runtime error (message in kep_last_error) */
-    KEP_EBREAKDOWN = 7,   /* reserved (Lanczos breakdown, NEXT f2/f3) */
-    KEP_ENOCONV = 8,      /* reserved (NEXT f2) */
-    KEP_ECLUSTER = 9,     /* reserved status, not an error */
+    KEP_EBREAKDOWN = 7,   /* Lanczos breakdown (reserved; kep_kth_eigenpair restarts instead) */
+    KEP_ENOCONV = 8,      /* stage 1 did not bracket lambda_k (kep_kth_eigenpair return), or, as a report
+                             status, stage 3 did not converge within max_si */
+    KEP_ECLUSTER = 9,     /* report status, not an error: stage 2 stopped on a cluster of
+                             > m_max eigenvalues in a 4-ulp interval */
     KEP_ENODEVICE = 10    /* no usable CUDA device */
 } kep_status;
 
@@ -156,7 +158,11 @@ KEP_API kep_status kep_analyze(int64_t n, const int64_t* colptr, const int32_t* 
                        const kep_opts* opts, kep_ctx** out);
 
 /* Values of A and B aligned with the analysed rowidx (nnz_lower each, host).
- * Copied to the device in assembly order.  Must precede kep_inertia. */
+ * Copied to the device in assembly order.  Must precede kep_inertia.  The
+ * pattern is recycled: new values (another pencil on the same pattern, e.g.
+ * the shifted pencils of PAPER.md:398-403 §3.3 "reuse the ordering and the
+ * symbolic factorization") need no new analysis (SPEC.md:50-58 shifted_combine
+ * on the union pattern).  Errors: KEP_EINVAL, KEP_ENODEVICE, KEP_ECUDA. */
 KEP_API kep_status kep_set_values(kep_ctx* ctx, const double* a, const double* b);
 
 /* Same, from device pointers (nnz_lower doubles each, on the ctx device). */
@@ -168,9 +174,12 @@ KEP_API kep_status kep_set_values_dev(kep_ctx* ctx, const double* a_dev, const d
  * info may be NULL. */
 KEP_API kep_status kep_inertia(kep_ctx* ctx, double sigma, int64_t* nu, kep_inertia_info* info);
 
-/* nu for m shifts (batched on the device, max_batch at a time).  nus[i] is
- * written when per_shift[i] == KEP_OK.  infos may be NULL.  Returns KEP_OK if
- * the call ran (individual shifts may be KEP_ESINGULAR), else the error. */
+/* nu for m shifts (batched on the device, max_batch at a time): the m
+ * evaluations of one multisection round, i.e. Alg. 1' line 3-4 (PAPER.md:
+ * 419-420) at P shifts at once (reading R12).
+ * sigmas[m], nus[m], per_shift[m] host arrays.  nus[i] is written when
+ * per_shift[i] == KEP_OK.  infos may be NULL.  Returns KEP_OK if the call ran
+ * (individual shifts may be KEP_ESINGULAR), else the error. */
 KEP_API kep_status kep_inertia_many(kep_ctx* ctx, int32_t m, const double* sigmas, int64_t* nus,
                             kep_status* per_shift, kep_inertia_info* infos);
 
@@ -219,7 +228,10 @@ KEP_API kep_status kep_factor_info(const kep_factorization* f, kep_factor_stats*
 
 /* x = (A - sigma B)^-1 b for nrhs right-hand sides (host, column-major,
  * leading dimensions ldb, ldx >= n; x may alias b).  Multifrontal forward
- * elimination, D^-1, back substitution.  Errors: KEP_EINVAL. */
+ * elimination, D^-1, back substitution: the shift-and-invert solves of Alg. 3
+ * (Eq. 2.4 at PAPER.md:146-151) and the B-solves of Alg. 2
+ * with the retained factor (SPEC.md:140-148 solve).
+ * Errors: KEP_EINVAL (bad sizes or a front beyond the solve kernels). */
 KEP_API kep_status kep_solve(const kep_factorization* f, int32_t nrhs, const double* b, int64_t ldb, double* x, int64_t ldx);
 
 /* Same for one right-hand side in device memory (n doubles each, dof order,
@@ -256,6 +268,10 @@ typedef struct {
                                    stage 2 stops when (sigma_u - sigma_l) / max(|sigma_l|, |sigma_u|) <
                                    bisect_rtol, lambda = the midpoint, no stage 3, x not written */
     double bisect_rtol;         /* default 1e-14 */
+    int32_t root_finder;        /* stage 2: 0 = bisection / multisection (Alg. 1', default); 1 = Brent's method
+                                   (zeroin: secant / inverse quadratic interpolation safeguarded by bisection)
+                                   on g(sigma) = nu_sigma - k + 1/2, the derivative-free bracketing root finder
+                                   of PAPER.md:110-115, :740-743 (one shift per iteration) */
 } kep_kth_opts;
 
 typedef struct {
@@ -270,6 +286,14 @@ typedef struct {
     double rel_diff;                    /* Eq. (3.5) at the last step */
     double seconds[3];                  /* wall time per stage */
     kep_status status;                  /* KEP_OK, KEP_ECLUSTER (cluster suspected), KEP_ENOCONV */
+    /* Table 6 analogue: first SI Lanczos iteration at which (3.3) and (3.4) held for
+       all m pairs ("Bound"), at which every relative residual was < tau_res ("Residual"), and every
+       relative difference (3.5) < tau_diff ("Difference"); 0 = never */
+    int32_t s3_iter_bound, s3_iter_residual, s3_iter_difference;
+    /* Fig. 4 / Table 5 analogue: the bracket after each stage-2 iteration (first 64) */
+    int32_t stage2_trace_len;
+    double stage2_trace_lower[64], stage2_trace_upper[64];
+    int64_t stage2_trace_m[64];         /* eigenvalues in the bracket, nu_u - nu_l */
 } kep_kth_report;
 
 KEP_API void kep_default_kth_opts(kep_kth_opts* o);
@@ -285,6 +309,12 @@ KEP_API void kep_default_kth_opts(kep_kth_opts* o);
  * be NULL. */
 KEP_API kep_status kep_kth_eigenpair(kep_ctx* ctx, int64_t k, const kep_kth_opts* opts, double* lambda, double* x,
                                      kep_kth_report* report);
+
+/* Testing hook: the host tridiagonal eigensolver of the Lanczos stages (Eq. (2.2),
+ * PAPER.md:129-134; Eq. (2.5)): T = tridiag(e, d, e) of order n
+ * (d[n], e[n-1]) = Z diag(w) Z^T, w ascending, Z column-major n x n (caller-owned).
+ * Implicit symmetric QR with the Wilkinson shift.  Errors: KEP_EINVAL, KEP_ENOCONV. */
+KEP_API kep_status kep_tridiag_eigen(int32_t n, const double* d, const double* e, double* w, double* Z);
 
 /* Analysis statistics (sizes, #nzf, flops per shift, memory). */
 KEP_API kep_status kep_get_analysis(const kep_ctx* ctx, kep_analysis_info* info);

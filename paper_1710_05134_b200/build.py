@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
            "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 SOURCES_CU = ["api.cu", "kernels.cu", "kernels_front.cu", "kernels_fast.cu", "kernels_solve.cu", "kth.cu", "kernels_resid.cu"]
-SOURCES_CPP = ["symbolic.cpp"]
+SOURCES_CPP = ["symbolic.cpp", "tridiag.cpp"]
 
 
 def _run(cmd, log):

@@ -519,6 +519,9 @@ kep_status upload_plan(kep_ctx* c, const int64_t* colptr, const int32_t* rowidx)
 
 // after a slack overflow: larger slack, new plan, re-upload the plan arrays that changed
 kep_status replan(kep_ctx* c, int slack) {
+    for (int64_t s = 0; s < c->sym.nf; ++s)                 // local positions are 16-bit (asm_rc, gather maps)
+        if ((int64_t)c->sym.forder[s] + slack > 65535)
+            return fail(c, KEP_ENOMEM, "delayed pivots grow a front beyond 65535 (16-bit local indices)");
     kep::plan_memory(c->sym, slack);
     cudaFree(c->d_cap);
     cudaFree(c->d_arena_off);
@@ -1415,12 +1418,74 @@ kep_status kep_kth_eigenpair(kep_ctx* c, int64_t k, const kep_kth_opts* opts_in,
         return nhi - nlo > o.m_max;                                          // Alg. 1' line 1
     };
     const int max_rounds = o.bisect_only ? std::max(o.max_bisect, 256) : o.max_bisect;
-    while (narrow_more()) {
+    auto trace = [&]() {                                                     // Fig. 4 / Table 5 analogue
+        if (R.stage2_trace_len < 64) {
+            R.stage2_trace_lower[R.stage2_trace_len] = lo;
+            R.stage2_trace_upper[R.stage2_trace_len] = hi;
+            R.stage2_trace_m[R.stage2_trace_len] = nhi - nlo;
+            R.stage2_trace_len++;
+        }
+    };
+    auto stalled = [&]() {
         if (R.stage2_rounds >= max_rounds ||
             (!o.bisect_only && hi - lo <= 4.0 * DBL_EPSILON * std::max(std::fabs(lo), std::fabs(hi)))) {
             R.status = o.bisect_only ? KEP_ENOCONV : KEP_ECLUSTER;
-            break;
+            return true;
         }
+        return false;
+    };
+    if (o.root_finder == 1) {
+        // Brent's method (zeroin) on g(sigma) = nu_sigma - k + 1/2: g < 0 at
+        // the lower end, > 0 at the upper end; b is the latest iterate, [b, c] always brackets lambda_k,
+        // a is the previous b.  Secant (a == c) or inverse quadratic interpolation, accepted only if it
+        // falls well inside the bracket and shrinks faster than the step before last; else bisection.
+        double a = lo, b = hi, c = lo;
+        double fa = (double)(nlo - k) + 0.5, fb = (double)(nhi - k) + 0.5, fc = fa;
+        int64_t na = nlo, nbb = nhi, nc = nlo;
+        double d = b - a, e = d;
+        for (;;) {
+            if (std::fabs(fc) < std::fabs(fb)) {
+                a = b; b = c; c = a;
+                fa = fb; fb = fc; fc = fa;
+                na = nbb; nbb = nc; nc = na;
+            }
+            lo = std::min(b, c); hi = std::max(b, c);
+            nlo = b < c ? nbb : nc; nhi = b < c ? nc : nbb;
+            if (R.stage2_rounds > 0) trace();
+            if (!narrow_more() || stalled()) break;
+            const double tol = 2.0 * DBL_EPSILON * std::fabs(b);
+            const double mm = 0.5 * (c - b);
+            if (std::fabs(e) >= tol && std::fabs(fa) > std::fabs(fb)) {
+                double p, q;
+                const double s = fb / fa;
+                if (a == c) {                                                // secant
+                    p = 2.0 * mm * s;
+                    q = 1.0 - s;
+                } else {                                                     // inverse quadratic
+                    q = fa / fc;
+                    const double r = fb / fc;
+                    p = s * (2.0 * mm * q * (q - r) - (b - a) * (r - 1.0));
+                    q = (q - 1.0) * (r - 1.0) * (s - 1.0);
+                }
+                if (p > 0.0) q = -q; else p = -p;
+                if (2.0 * p < std::min(3.0 * mm * q - std::fabs(tol * q), std::fabs(e * q))) { e = d; d = p / q; }
+                else { d = mm; e = mm; }
+            } else {
+                d = mm;
+                e = mm;
+            }
+            a = b; fa = fb; na = nbb;
+            b += std::fabs(d) > tol ? d : (mm > 0.0 ? tol : -tol);
+            kep_status st = nu_at(b, nbb);
+            if (st != KEP_OK) return st;
+            fb = (double)(nbb - k) + 0.5;
+            R.stage2_rounds++;
+            R.stage2_shifts++;
+            if ((fb > 0.0) == (fc > 0.0)) { c = a; fc = fa; nc = na; d = e = b - a; }
+        }
+    }
+    while (o.root_finder != 1 && narrow_more()) {
+        if (stalled()) break;
         for (int i = 0; i < P; ++i) sg[i] = lo + (hi - lo) * (double)(i + 1) / (double)(P + 1);
         kep_status st = kep_inertia_many(c, P, sg.data(), nv.data(), ps.data(), nullptr);
         if (st != KEP_OK) return st;
@@ -1440,6 +1505,7 @@ kep_status kep_kth_eigenpair(kep_ctx* c, int64_t k, const kep_kth_opts* opts_in,
             if (na < k && k <= nbb) { l2 = sa; h2 = sb; nl2 = na; nh2 = nbb; break; }
         }
         lo = l2; hi = h2; nlo = nl2; nhi = nh2;
+        trace();
     }
     R.sigma_lower = lo; R.sigma_upper = hi; R.nu_lower = nlo; R.nu_upper = nhi;
     R.seconds[1] = now_s() - t0;
@@ -1467,6 +1533,8 @@ kep_status kep_kth_eigenpair(kep_ctx* c, int64_t k, const kep_kth_opts* opts_in,
     if (!F) return fail(c, KEP_ESINGULAR, "stage-3 shift stays singular");
     R.sigma_si = sigma;
     const int J3 = std::max<int>(o.max_si, (int)m);
+    if ((size_t)(J3 + 1) * (size_t)m * sizeof(double) > 200 * 1024)        // k_ritz stages C (j x m) in shared memory
+        return fail(c, KEP_EINVAL, "max_si * m_max too large for the Ritz-vector kernel");
     DevVec W, Vt, X, Xp, g, Cm, ta, tb;
     KEP_CUDA(c, cudaMalloc(&ta.p, sizeof(double) * n));                  // scratch of the convergence tests
     KEP_CUDA(c, cudaMalloc(&tb.p, sizeof(double) * n));
@@ -1528,21 +1596,27 @@ kep_status kep_kth_eigenpair(kep_ctx* c, int64_t k, const kep_kth_opts* opts_in,
             KEP_CUDA(c, cudaMemcpyAsync(Cm.p, Ch.data(), sizeof(double) * Ch.size(), cudaMemcpyHostToDevice, c->stream));
             KEP_CUDA(c, cudaMemcpyAsync(g.p, gh.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
             kep::launch_ritz(W.p, n, j, Cm.p, r.p, g.p, (int)m, X.p, n, n, c->stream);   // x_{i,2}, Eq. (2.7)
-            bool conv = inc && dis && have_prev;
-            for (int q = 0; q < m; ++q) {
-                if (!conv) break;
+            KEP_CUDA(c, cudaGetLastError());
+            if (inc && dis && !R.s3_iter_bound) R.s3_iter_bound = j;                // Table 6 "Bound"
+            bool all_res = inc && dis, all_dif = inc && dis && have_prev;
+            for (int q = 0; q < m && inc && dis; ++q) {                       // every pair: Table 6 columns
                 double* xq = X.p + (size_t)q * n;
                 const double xx = L.dot(xq, xq);
                 L.spmv(xq, ta.p, tb.p);                                       // (A - lambda B) x
                 kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 1.0, ta.p, -lam[q], tb.p, 0.0, nullptr, n, c->stream);
                 hres[q] = std::sqrt(L.dot(ta.p, ta.p) / xx);
+                all_res = all_res && hres[q] < o.tau_res;
+                if (!have_prev) continue;
                 double* xpq = Xp.p + (size_t)q * n;
                 const double pp = L.dot(xpq, xpq), xp = L.dot(xq, xpq);
                 const double sc = (xp < 0 ? -1.0 : 1.0) * std::sqrt(pp / xx);      // equal 2-norms, aligned signs
                 kep::launch_combine(nullptr, 0, 0, nullptr, 0.0, 0.0, ta.p, sc, xq, -1.0, xpq, n, c->stream);
                 hdif[q] = std::sqrt(L.dot(ta.p, ta.p) / pp);                       // Eq. (3.5)
-                conv = conv && hres[q] < o.tau_res && hdif[q] < o.tau_diff;
+                all_dif = all_dif && hdif[q] < o.tau_diff;
             }
+            if (all_res && !R.s3_iter_residual) R.s3_iter_residual = j;
+            if (all_dif && !R.s3_iter_difference) R.s3_iter_difference = j;
+            const bool conv = inc && dis && have_prev && all_res && all_dif;
             KEP_CUDA(c, cudaMemcpyAsync(Xp.p, X.p, sizeof(double) * n * m, cudaMemcpyDeviceToDevice, c->stream));
             have_prev = true;
             if (conv) {

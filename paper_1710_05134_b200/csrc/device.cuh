@@ -116,6 +116,16 @@ __device__ __forceinline__ void pair_eig(double d11, double d21, double d22, dou
 // (arena offsets are 256-byte aligned) and the GEMM kernels stage with 16-byte copies.
 __host__ __device__ __forceinline__ int ldpad(int f) { return (f + 1) & ~1; }
 
+// Shared-memory opt-in (cudaFuncSetAttribute) applies per device: `mask` holds one bit per
+// device ordinal; returns true the first time it is called for the current device.
+inline bool first_on_device(unsigned long long& mask) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    const unsigned long long old = __atomic_fetch_or(&mask, bit, __ATOMIC_ACQ_REL);
+    return (old & bit) == 0;
+}
+
 __device__ __forceinline__ void atomic_max_pos_double(unsigned long long* addr, double v) {
     atomicMax(addr, (unsigned long long)__double_as_longlong(v));
 }

@@ -776,11 +776,11 @@ __global__ void k_reset_stats(ShiftStat* st, int batch) {
 void launch_assemble(const DevPlan& P, const int4* items, int nitems, int batch, bool only_flagged, cudaStream_t st) {
     if (nitems <= 0) return;
     const size_t smem = sizeof(double) * kAsmNW * kAsmChunk;
-    static bool attr = false;                 // static + dynamic shared memory above 48 KB: opt in
-    if (!attr) {
+    static unsigned long long attr = 0;                 // static + dynamic shared memory above 48 KB: opt in
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_reassemble, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+        
     }
     if (only_flagged) k_reassemble<<<dim3(nitems, batch), kAsmThreads, smem, st>>>(P, items);
     else k_assemble<<<dim3(nitems, batch), kAsmThreads, smem, st>>>(P, items);

@@ -217,8 +217,8 @@ bool schur_small_ok(int c, int qcap) { return c > 0 && c <= SS_C && qcap <= SS_K
 void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
     if (nfronts <= 0) return;
     const size_t smem = sizeof(double) * SS_C * SS_P;
-    static bool attr = false;
-    if (!attr) { cudaFuncSetAttribute(k_schur_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) { cudaFuncSetAttribute(k_schur_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  }
     k_schur_small<<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts);
 }
 }  // namespace kep

@@ -1145,10 +1145,10 @@ int fs_iters(int qmax, int64_t nblocks) {
 template <int NB, int TH, bool GLS>
 void launch_fsp_t(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int RS, size_t smem, int mode,
                   cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(k_fsp<NB, TH, GLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmemLimit);
-        attr = true;
+        
     }
     k_fsp<NB, TH, GLS><<<dim3(nfronts, batch), TH, smem, st>>>(P, fronts, RS, mode);
 }
@@ -1193,12 +1193,12 @@ void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, int 
     if (nitems <= 0) return;
     const size_t smem = sizeof(double) * (LST * LR * BP + LST * LB * BP + LR * (LB + 1));
     const size_t smem_s = sizeof(double) * (LR * (LB + 1) + LB * (LB + 1));
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(k_l21<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_l21<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
         cudaFuncSetAttribute(k_l21<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+        
     }
     if (mode == 1) k_l21<1><<<dim3(nitems, batch), LT, smem_s, st>>>(P, items);
     else if (mode == 2) k_l21<2><<<dim3(nitems, batch), LT, smem, st>>>(P, items);
@@ -1216,8 +1216,8 @@ int64_t l21_x_doubles(int qcap) { return (int64_t)2 * LB * LB * ((qcap + LB - 2)
 void launch_l21x_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
     if (nfronts <= 0) return;
     const size_t smem = sizeof(double) * XPW * LB * (LB + 1);
-    static bool attr = false;
-    if (!attr) { cudaFuncSetAttribute(k_l21x_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) { cudaFuncSetAttribute(k_l21x_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  }
     k_l21x_prep<<<dim3(nfronts, batch), XPW * 32, smem, st>>>(P, fronts);
 }
 

@@ -161,11 +161,10 @@ void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, i
 }
 
 static void set_smem_attr() {
-    static bool done = false;
-    if (done) return;
+    static unsigned long long done = 0;
+    if (!first_on_device(done)) return;
     cudaFuncSetAttribute(k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    done = true;
 }
 
 int solve_max_front() { return 200 * 1024 / 8; }

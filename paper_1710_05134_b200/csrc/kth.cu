@@ -153,74 +153,9 @@ void launch_combine(const double* V, int64_t ldv, int j, const double* c, double
 void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const double* r, const double* g, int m,
                  double* X, int64_t ldx, int64_t n, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)j * m + m);
-    static bool attr = false;
-    if (!attr) { cudaFuncSetAttribute(k_ritz, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); attr = true; }
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) { cudaFuncSetAttribute(k_ritz, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);  }
     k_ritz<<<grid_for(n), VT, smem, st>>>(W, ldw, j, C, r, g, m, X, ldx, n);
-}
-
-// ---------------------------------------------------------------- host: symmetric tridiagonal eigenproblem
-// Implicit-shift QL (the classical tql2 scheme) on T = tridiag(e, d, e):
-// eigenvalues ascending in d, eigenvectors as columns of Z (column-major n x n).
-bool tridiag_eigen(std::vector<double>& d, std::vector<double> e, std::vector<double>& Z) {
-    const int n = (int)d.size();
-    Z.assign((size_t)n * n, 0.0);
-    for (int i = 0; i < n; ++i) Z[i + (size_t)i * n] = 1.0;
-    e.resize(n, 0.0);
-    for (int i = 1; i < n; ++i) e[i - 1] = e[i - 1];
-    e[n - 1] = 0.0;
-    for (int l = 0; l < n; ++l) {
-        int iter = 0, m;
-        do {
-            for (m = l; m < n - 1; ++m) {
-                const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
-                if (std::fabs(e[m]) <= DBL_EPSILON * dd) break;
-            }
-            if (m != l) {
-                if (iter++ == 60) return false;
-                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-                double r = std::hypot(g, 1.0);
-                g = d[m] - d[l] + e[l] / (g + (g >= 0 ? std::fabs(r) : -std::fabs(r)));
-                double s = 1.0, c = 1.0, p = 0.0;
-                int i;
-                for (i = m - 1; i >= l; --i) {
-                    double f = s * e[i], b = c * e[i];
-                    e[i + 1] = (r = std::hypot(f, g));
-                    if (r == 0.0) {
-                        d[i + 1] -= p;
-                        e[m] = 0.0;
-                        break;
-                    }
-                    s = f / r;
-                    c = g / r;
-                    g = d[i + 1] - p;
-                    r = (d[i] - g) * s + 2.0 * c * b;
-                    d[i + 1] = g + (p = s * r);
-                    g = c * r - b;
-                    for (int k = 0; k < n; ++k) {
-                        f = Z[k + (size_t)(i + 1) * n];
-                        Z[k + (size_t)(i + 1) * n] = s * Z[k + (size_t)i * n] + c * f;
-                        Z[k + (size_t)i * n] = c * Z[k + (size_t)i * n] - s * f;
-                    }
-                }
-                if (r == 0.0 && i >= l) continue;
-                d[l] -= p;
-                e[l] = g;
-                e[m] = 0.0;
-            }
-        } while (m != l);
-    }
-    // sort ascending
-    std::vector<int> idx(n);
-    std::iota(idx.begin(), idx.end(), 0);
-    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a] < d[b]; });
-    std::vector<double> d2(n), Z2((size_t)n * n);
-    for (int q = 0; q < n; ++q) {
-        d2[q] = d[idx[q]];
-        std::memcpy(&Z2[(size_t)q * n], &Z[(size_t)idx[q] * n], sizeof(double) * n);
-    }
-    d.swap(d2);
-    Z.swap(Z2);
-    return true;
 }
 
 }  // namespace kep

@@ -67,7 +67,7 @@ class _KthOpts(C.Structure):
                 ("max_lanczos", C.c_int32), ("max_bisect", C.c_int32), ("max_si", C.c_int32),
                 ("shifts_per_round", C.c_int32), ("seed", C.c_uint64),
                 ("v0_stage1", C.POINTER(C.c_double)), ("v0_stage3", C.POINTER(C.c_double)),
-                ("bisect_only", C.c_int32), ("bisect_rtol", C.c_double)]
+                ("bisect_only", C.c_int32), ("bisect_rtol", C.c_double), ("root_finder", C.c_int32)]
 
 
 class _KthReport(C.Structure):
@@ -76,7 +76,10 @@ class _KthReport(C.Structure):
                 ("nu_lower", C.c_int64), ("nu_upper", C.c_int64), ("sigma_si", C.c_double),
                 ("stage1_iters", C.c_int32), ("stage2_rounds", C.c_int32), ("stage2_shifts", C.c_int32),
                 ("stage3_iters", C.c_int32), ("eta", C.c_double), ("rel_residual", C.c_double),
-                ("rel_diff", C.c_double), ("seconds", C.c_double * 3), ("status", C.c_int)]
+                ("rel_diff", C.c_double), ("seconds", C.c_double * 3), ("status", C.c_int),
+                ("s3_iter_bound", C.c_int32), ("s3_iter_residual", C.c_int32), ("s3_iter_difference", C.c_int32),
+                ("stage2_trace_len", C.c_int32), ("stage2_trace_lower", C.c_double * 64),
+                ("stage2_trace_upper", C.c_double * 64), ("stage2_trace_m", C.c_int64 * 64)]
 
 
 _lib = None
@@ -121,6 +124,8 @@ def lib():
         L.kep_solve_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.kep_factor_export.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_double), P(C.c_double), P(C.c_int64),
                                         P(C.c_int32), P(C.c_double)]
+        L.kep_tridiag_eigen.argtypes = [C.c_int32, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double)]
+        L.kep_tridiag_eigen.restype = C.c_int
         L.kep_factor_residual.argtypes = [C.c_void_p, C.c_double, P(C.c_double), P(C.c_double)]
         L.kep_factor_residual.restype = C.c_int
         L.kep_factor_destroy.argtypes = [C.c_void_p]
@@ -281,7 +286,7 @@ class Kep:
 
     def kth_eigenpair(self, k: int, m_max=20, tau_res=1e-10, tau_diff=1e-10, max_lanczos=64, max_bisect=128,
                       max_si=500, shifts_per_round=1, seed=1, v0_stage1=None, v0_stage3=None, want_x=True,
-                      bisect_only=False, bisect_rtol=1e-14):
+                      bisect_only=False, bisect_rtol=1e-14, root_finder="bisection"):
         """kep_kth_eigenpair: (lambda_k or None, x or None, report dict)."""
         o = _KthOpts()
         lib().kep_default_kth_opts(C.byref(o))
@@ -289,6 +294,7 @@ class Kep:
         o.max_lanczos, o.max_bisect, o.max_si = int(max_lanczos), int(max_bisect), int(max_si)
         o.shifts_per_round, o.seed = int(shifts_per_round), int(seed)
         o.bisect_only, o.bisect_rtol = int(bool(bisect_only)), float(bisect_rtol)
+        o.root_finder = {"bisection": 0, "brent": 1}[root_finder]
         keep = []
         for name, v in (("v0_stage1", v0_stage1), ("v0_stage3", v0_stage3)):
             if v is not None:
@@ -303,8 +309,20 @@ class Kep:
                                      _ptr(x, C.c_double) if want_x else C.cast(None, C.POINTER(C.c_double)),
                                      C.byref(rp))
         self._check(st)
-        rep = {f: getattr(rp, f) for f, _ in _KthReport._fields_ if f != "seconds"}
+        arrays = ("seconds", "stage2_trace_lower", "stage2_trace_upper", "stage2_trace_m")
+        rep = {f: getattr(rp, f) for f, _ in _KthReport._fields_ if f not in arrays}
         rep["seconds"] = list(rp.seconds)
+        nt = rp.stage2_trace_len
+        rep["stage2_trace"] = [(rp.stage2_trace_lower[i], rp.stage2_trace_upper[i], rp.stage2_trace_m[i])
+                               for i in range(nt)]
+        # Table 4 / Table 5 analogues: length, index range, m, gap
+        for tag, a, b, na, nb in (("table4", rp.s1_lower, rp.s1_upper, rp.s1_nu_lower, rp.s1_nu_upper),
+                                  ("table5", rp.sigma_lower, rp.sigma_upper, rp.nu_lower, rp.nu_upper)):
+            m = nb - na
+            rep[tag] = dict(interval=(a, b), length=b - a, index_range=(na + 1, nb), m=m,
+                            gap=(b - a) / m if m > 0 else None)
+        rep["table6"] = dict(m=rp.nu_upper - rp.nu_lower, bound=rp.s3_iter_bound, residual=rp.s3_iter_residual,
+                             difference=rp.s3_iter_difference)
         ok = rp.status == KEP_OK
         return (lam.value if ok else None), (x if ok and not bisect_only else None), rep
 
@@ -320,6 +338,22 @@ class Kep:
         order = np.empty(nf, dtype=np.int64)
         self._check(lib().kep_get_fronts(self._h, _ptr(first, C.c_int64), _ptr(parent, C.c_int64), _ptr(order, C.c_int64)))
         return first, parent, order
+
+
+def tridiag_eigen(d, e):
+    """kep_tridiag_eigen (testing hook): eigenvalues (ascending) and eigenvectors of tridiag(e, d, e)."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    e = np.ascontiguousarray(e, dtype=np.float64)
+    n = d.shape[0]
+    assert e.shape == (max(n - 1, 0),)
+    w = np.empty(n)
+    Z = np.empty((n, n), order="F")
+    ee = e if n > 1 else np.zeros(1)
+    st = lib().kep_tridiag_eigen(n, _ptr(d, C.c_double), _ptr(ee, C.c_double), _ptr(w, C.c_double),
+                                 _ptr(Z, C.c_double))
+    if st != KEP_OK:
+        raise KepError(st, "kep_tridiag_eigen")
+    return w, Z
 
 
 def version() -> str:

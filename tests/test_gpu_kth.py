@@ -125,3 +125,50 @@ def test_c1_straightforward_bisection(kk, P):
             it += 1
         assert abs(it - rep["stage2_rounds"]) <= 2
         assert abs(0.5 * (lo + hi) - lam) <= 1e-13 * abs(lam)
+
+
+@pytest.mark.parametrize("kk", [37, 300, 812])
+def test_c1_brent_stage2(kk):
+    """f4: Brent's method on nu in stage 2.  The GPU driver takes the
+    oracle's Brent steps exactly (same counts -> same iterates), brackets lambda_k with <= m_max
+    eigenvalues, and the validated eigenpair is the same as with bisection."""
+    p = kepgen.config(1)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    v1, v3 = _start(p.n, 11), _start(p.n, 12)
+    lam, x, rep = k.kth_eigenpair(kk, root_finder="brent", v0_stage1=v1, v0_stage3=v3)
+    assert rep["status"] == KEP_OK, rep
+    assert abs(lam - w[kk - 1]) <= 1e-10 * abs(w[kk - 1])
+    nu = lambda s: oracle.nu_eig(A, B, s, eigvals=w)
+    (l2, h2, nl2, nh2), it, tr = oracle.bisection.brent_nu(nu, kk, rep["s1_lower"], rep["s1_upper"],
+                                                            rep["s1_nu_lower"], rep["s1_nu_upper"], m_max=20)
+    assert rep["stage2_rounds"] == it and (rep["nu_lower"], rep["nu_upper"]) == (nl2, nh2)
+    assert np.isclose(rep["sigma_lower"], l2, rtol=1e-12) and np.isclose(rep["sigma_upper"], h2, rtol=1e-12)
+    assert [m for (_, _, m) in rep["stage2_trace"]][-1] == nh2 - nl2
+    lam_b, _, rep_b = k.kth_eigenpair(kk, v0_stage1=v1, v0_stage3=v3)
+    assert abs(lam_b - lam) <= 1e-11 * abs(lam)
+
+
+def test_c1_report_tables():
+    """Table 4/5/6 analogues in the report: intervals, index ranges, m, gap,
+    and the SI Lanczos iteration counts Bound <= Residual, Bound <= Difference <= stage3_iters."""
+    p = kepgen.config(1)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    k = Kep.from_pencil(p)
+    k.set_values(p.a, p.b)
+    lam, x, rep = k.kth_eigenpair(300, v0_stage1=_start(p.n, 11), v0_stage3=_start(p.n, 12))
+    t4, t5, t6 = rep["table4"], rep["table5"], rep["table6"]
+    for t in (t4, t5):
+        lo, hi = t["interval"]
+        i0, i1 = t["index_range"]
+        assert i0 == int(np.sum(w < lo)) + 1 and i1 == int(np.sum(w < hi)) and t["m"] == i1 - i0 + 1
+        assert np.isclose(t["gap"], (hi - lo) / t["m"])
+    assert t5["m"] <= 20 and t5["length"] < t4["length"]
+    tr = rep["stage2_trace"]
+    assert len(tr) == rep["stage2_rounds"] and tr[-1][2] == t5["m"]
+    assert all(a >= b for (_, _, a), (_, _, b) in zip(tr, tr[1:]))              # m never grows
+    assert 0 < t6["bound"] <= t6["residual"] <= rep["stage3_iters"]
+    assert t6["bound"] < t6["difference"] <= rep["stage3_iters"]

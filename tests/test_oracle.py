@@ -299,3 +299,27 @@ def test_blocked_sparse_oracle_twin_mid_size():
     so = oracle.SparseOracle(q)
     for s in kepgen.uniform_shifts(w[0], w[-1], 5):
         assert so.inertia(s, nb=32).n_neg == oracle.nu_twin(q.meta["twin"], s, w)
+
+
+# ---------------------------------------------------------------- f4: Brent's method on nu
+def test_brent_nu_brackets_kth():
+    from oracle.bisection import bisect_alg1p, brent_nu
+    g = json.load(open(GOLD))["bisection"][0]                    # SPEC diag(1..64), B = I
+    A = np.diag(np.arange(1, g["n"] + 1, dtype=float))
+    B = np.eye(g["n"])
+    nu = lambda s: oracle.nu_dense(A, B, s).n_neg
+    for k in (1, 17, 32, 64):
+        for m_max in (1, 4, 20):
+            (lo, hi, nl, nh), it, tr = brent_nu(nu, k, 0.5, 64.5, 0, 64, m_max=m_max)
+            assert nl < k <= nh and nh - nl <= m_max and lo <= k < hi      # lambda_k in [lo, hi)
+            assert nl == nu(lo) and nh == nu(hi)
+    # a clustered random pencil against eigh (P1): the bracket holds lambda_k, <= m_max eigenvalues
+    rng = np.random.default_rng(9)
+    Aa, Bb = _rand_pencil(rng, 120)
+    w = oracle.eigvals_pencil(Aa, Bb)
+    nu2 = lambda s: oracle.nu_eig(Aa, Bb, s, eigvals=w)
+    for k in (5, 60, 118):
+        (lo, hi, nl, nh), it, _ = brent_nu(nu2, k, w[0] - 1, w[-1] + 1, 0, 120, m_max=3)
+        assert lo <= w[k - 1] < hi and nh - nl <= 3 and nl == int(np.sum(w < lo))
+        _, it_b, _ = bisect_alg1p(nu2, k, w[0] - 1, w[-1] + 1, 0, 120, m_max=3)
+        assert it <= 3 * it_b + 3
