@@ -146,7 +146,7 @@ def test_c1_brent_stage2(kk):
                                                             rep["s1_nu_lower"], rep["s1_nu_upper"], m_max=20)
     assert rep["stage2_rounds"] == it and (rep["nu_lower"], rep["nu_upper"]) == (nl2, nh2)
     assert np.isclose(rep["sigma_lower"], l2, rtol=1e-12) and np.isclose(rep["sigma_upper"], h2, rtol=1e-12)
-    assert [m for (_, _, m) in rep["stage2_trace"]][-1] == nh2 - nl2
+    assert len(rep["stage2_trace"]) == it and (it == 0 or rep["stage2_trace"][-1][2] == nh2 - nl2)
     lam_b, _, rep_b = k.kth_eigenpair(kk, v0_stage1=v1, v0_stage3=v3)
     assert abs(lam_b - lam) <= 1e-11 * abs(lam)
 
