@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <ctime>
@@ -93,6 +94,10 @@ struct kep_ctx {
     int64_t gscratch_stride = 0;
     double* d_gscratch = nullptr;
     std::vector<int64_t> uitem_off, uitem_cnt, small_off, small_cnt;
+    // k_small (whole FS panel in shared memory): per level list offsets, shared-memory cap, threads
+    int32_t* d_smfronts = nullptr;
+    struct SmGroup { int64_t off, cnt; int cap, th; };
+    std::vector<std::vector<SmGroup>> sm_groups;    // per level: size classes of the k_small fronts
     int32_t* d_small = nullptr;                  // fronts whose Schur update runs in k_schur_small
     std::vector<int> level_qmax;                // per level: max p + slack over its fast fronts
     std::vector<double> item_flops;             // per level: algorithmic a4 flops of its fast fronts
@@ -106,6 +111,8 @@ struct kep_ctx {
     kep_profile prof;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<int> ev_class;
+    std::vector<int> ev_level;
+    std::vector<std::array<double, KEP_K_NCLASS>> lvl_ms;    // KEP_PROFILE_LEVELS: per level and class
 };
 
 // Retained factors of one shift.
@@ -137,6 +144,10 @@ namespace {
 
 thread_local std::string g_err;
 constexpr int kReruns = 2;      // fast-path reruns per level before the unblocked fallback
+constexpr int kSmallDelay = 8;  // k_small eligibility: the panel with this many delayed-in columns fits kSmallCap
+constexpr int kSmallMaxPiv = 16;   // k_small: fronts with at most this many own pivots
+constexpr int kSmallPlan = 2;   // k_small size class: planned delayed-in columns (more, beyond the class cap: k_factor_ref)
+constexpr int64_t kSmallCap = 24 * 1024;   // k_small: FS panel budget in doubles (192 KB of shared memory)
 
 kep_status fail(kep_ctx* c, kep_status s, const std::string& msg) {
     if (c) c->err = msg;
@@ -217,10 +228,20 @@ kep_status build_lists(kep_ctx* c) {
     const Symbolic& S = c->sym;
     // fast (blocked) path, or the unblocked kernel (variant 1; FS blocks beyond the fast kernels)
     // (routing tiny fronts to the unblocked kernel measured slower at c4: its fronts live in HBM)
+    // k_small: the FS panel (f x (p + kSmallDelay)) fits the shared-memory budget (non-root fronts)
+    const bool use_small = c->opts.kernel_variant == 0 && !getenv("KEP_NO_SMALL");
+    auto is_small = [&](int s) {
+        const int64_t qq = (int64_t)S.npiv[s] + kSmallDelay;
+        // (measured at c4: faster than the k_fsp/k_l21/k_check path up to ~16 pivots, slower beyond)
+        return use_small && S.ncb[s] > 0 && S.npiv[s] <= kSmallMaxPiv && (int64_t)S.forder[s] * qq <= kSmallCap;
+    };
     auto is_fast = [&](int s) {
-        return c->opts.kernel_variant == 0 && kep::front_nb_for(S.capacity[s] - S.ncb[s]) > 0;
+        return c->opts.kernel_variant == 0 && !is_small(s) && kep::front_nb_for(S.capacity[s] - S.ncb[s]) > 0;
     };
     const int nl = (int)S.level_ptr.size() - 1;
+    std::vector<int32_t> smf;
+    c->sm_groups.assign(nl, {});
+    c->item_flops.assign(nl, 0.0);
     std::vector<int32_t> fast, ref;
     std::vector<int4> items, litems, lsitems, lxitems, uitems;
     std::vector<int32_t> xfronts;
@@ -278,10 +299,42 @@ kep_status build_lists(kep_ctx* c) {
                 rd2[s].z = (int)aitems.size() - rd2[s].y;
             }
         c->raitem_cnt[L] = (int64_t)aitems.size() - c->raitem_off[L];
+        // k_small fronts in size classes (shared memory per launch = the class cap: occupancy).  The
+        // class is chosen for kSmallPlan delayed-in columns; a front with more is handed to k_factor_ref.
+        {
+            static const int kCls[8] = {1536, 2048, 3072, 4096, 6144, 8192, 12288, (int)kSmallCap};
+            int kTh[8] = {32, 64, 64, 128, 128, 256, 256, 256};
+            if (const char* e = getenv("KEP_SMALL_TH"))         // tuning: threads per size class
+                sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d", &kTh[0], &kTh[1], &kTh[2], &kTh[3], &kTh[4], &kTh[5], &kTh[6],
+                       &kTh[7]);
+            for (int cl = 0; cl < 8; ++cl) {
+                kep_ctx::SmGroup g{(int64_t)smf.size(), 0, kCls[cl], kTh[cl]};
+                for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
+                    const int s = S.level_fronts[k];
+                    if (!is_small(s)) continue;
+                    const int64_t need = (int64_t)S.forder[s] * (S.npiv[s] + kSmallPlan);
+                    if (need <= kCls[cl] && (cl == 0 || need > kCls[cl - 1])) smf.push_back(s);
+                }
+                g.cnt = (int64_t)smf.size() - g.off;
+                if (g.cnt) c->sm_groups[L].push_back(g);
+            }
+        }
         // tile lists in the level's front order
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
             const int s = S.level_fronts[k];
             const int qcap = S.capacity[s] - S.ncb[s];            // p + slack
+            if (is_small(s)) {                                     // k_small, then the Schur tiles
+                const int qq = S.npiv[s] + kSmallDelay;
+                if (kep::schur_small_ok(S.ncb[s], qq)) {
+                    small.push_back(s);
+                } else {
+                    const int nt = (S.ncb[s] + 63) / 64;
+                    for (int I = 0; I < nt; ++I)
+                        for (int J = 0; J <= I; ++J) items.push_back(make_int4(s, I, J, 0));
+                }
+                c->item_flops[L] += (double)S.npiv[s] * (double)S.ncb[s] * (double)(S.ncb[s] + 1);
+                continue;
+            }
             if (!is_fast(s)) {
                 ref.push_back(s);
                 continue;
@@ -369,7 +422,6 @@ kep_status build_lists(kep_ctx* c) {
         mx_a = std::max(mx_a, c->raitem_cnt[L]);
         c->small_cnt[L] = (int64_t)small.size() - c->small_off[L];
     }
-    c->item_flops.assign(nl, 0.0);
     for (int L = 0; L < nl; ++L)
         for (int64_t k = c->fast_off[L]; k < c->fast_off[L] + c->fast_cnt[L]; ++k) {
             const int s = fast[k];
@@ -386,6 +438,8 @@ kep_status build_lists(kep_ctx* c) {
     KEP_CUDA(c, upload(&c->d_uitems, uitems));
     cudaFree(c->d_small); c->d_small = nullptr;
     KEP_CUDA(c, upload(&c->d_small, small));
+    cudaFree(c->d_smfronts); c->d_smfronts = nullptr;
+    KEP_CUDA(c, upload(&c->d_smfronts, smf));
     cudaFree(c->d_aux_off); c->d_aux_off = nullptr;
     KEP_CUDA(c, upload(&c->d_litems, litems));
     cudaFree(c->d_lsitems); c->d_lsitems = nullptr;
@@ -642,6 +696,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
         const int nl = (int)S.level_ptr.size() - 1;
         const bool prof = c->opts.profile != 0;
         size_t nev = 0;
+        int cur_level = 0;
         auto mark = [&](int cls, bool begin) {
             if (!prof) return;
             if (nev >= c->ev_pool.size()) {
@@ -649,18 +704,31 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 cudaEventCreate(&ev);
                 c->ev_pool.push_back(ev);
                 c->ev_class.push_back(0);
+                c->ev_level.push_back(0);
             }
             cudaEventRecord(c->ev_pool[nev], c->stream);
             c->ev_class[nev] = begin ? cls : -1;
+            c->ev_level[nev] = cur_level;
             ++nev;
         };
         for (int L = 0; L < nl; ++L) {
             const int b = S.level_ptr[L], nfl = S.level_ptr[L + 1] - b;
+            cur_level = L;
             mark(KEP_K_ASSEMBLE, true);
             if (c->asm_red[L]) kep::launch_assemble_red(P, c->d_level_fronts + b, nfl, m, c->stream);
             else kep::launch_assemble(P, c->d_aitems + c->aitem_off[L], (int)c->aitem_cnt[L], m, false, c->stream);
             mark(KEP_K_ASSEMBLE, false);
             if (resid) kep::launch_capture(P, c->d_level_fronts + b, nfl, c->d_f0, c->stream);
+            for (const auto& g : c->sm_groups[L]) {         // whole-panel fronts; overflow -> unblocked kernel
+                mark(KEP_K_PANEL, true);
+                kep::launch_small(P, c->d_smfronts + g.off, (int)g.cnt, m, g.cap, g.th, c->stream);
+                mark(KEP_K_PANEL, false);
+                mark(KEP_K_REF, true);
+                kep::launch_factor_list(P, c->d_smfronts + g.off, (int)g.cnt, m, c->stream, true);
+                mark(KEP_K_REF, false);
+                c->prof.launches[KEP_K_PANEL]++;
+                c->prof.launches[KEP_K_REF]++;
+            }
             c->prof.launches[KEP_K_ASSEMBLE]++;
             if (c->fast_cnt[L]) {
                 const int32_t* fl = c->d_lists + c->fast_off[L];
@@ -787,6 +855,8 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             float ms = 0.f;
             cudaEventElapsedTime(&ms, c->ev_pool[x], c->ev_pool[x + 1]);
             c->prof.ms[c->ev_class[x]] += ms;
+            if ((int)c->lvl_ms.size() <= c->ev_level[x]) c->lvl_ms.resize(c->ev_level[x] + 1, {});
+            c->lvl_ms[c->ev_level[x]][c->ev_class[x]] += ms;
         }
         c->prof.shifts += m;
         c->prof.factor_flops += c->sym.flops * m;
@@ -1080,7 +1150,7 @@ kep_status kep_factor_residual(kep_ctx* c, double sigma, double* bound, double* 
         if (const char* dump = getenv("KEP_DEBUG_DUMP")) {      // one front: F0, arena, perm, store
             const int64_t s2 = atoll(dump);
             const int4 h = hdr[s2];
-            const int f = h.y, ld = kep::ldpad(f), q = h.z, e = h.x;
+            const int f = h.y, ld = kep::ldpad(S.capacity[s2]), q = h.z, e = h.x;
             std::vector<double> f0((size_t)f * ld), fa((size_t)f * ld), pan((size_t)f * e);
             std::vector<double> aux((size_t)(S.capacity[s2] - S.ncb[s2]) * kep::AUX_W);
             std::vector<int64_t> aoff(S.nf);
@@ -1683,6 +1753,7 @@ kep_status kep_get_profile(const kep_ctx* c, kep_profile* p) {
 }
 
 kep_status kep_reset_profile(kep_ctx* c) {
+    if (c) c->lvl_ms.clear();
     if (!c) return KEP_EINVAL;
     std::memset(&c->prof, 0, sizeof(c->prof));
     return KEP_OK;
@@ -1708,6 +1779,16 @@ kep_status kep_get_fronts(const kep_ctx* c, int64_t* first, int64_t* parent, int
 
 void kep_destroy(kep_ctx* c) {
     if (!c) return;
+    if (getenv("KEP_PROFILE_LEVELS") && !c->lvl_ms.empty()) {
+        fprintf(stderr, "[kep] per-level kernel ms (assemble fs ref schur l21 check fsu) fronts maxf\n");
+        for (size_t L = 0; L < c->lvl_ms.size(); ++L) {
+            int mx = 0;
+            for (int x = c->sym.level_ptr[L]; x < c->sym.level_ptr[L + 1]; ++x) mx = std::max(mx, (int)c->sym.forder[c->sym.level_fronts[x]]);
+            fprintf(stderr, "[kep] L%2zu", L);
+            for (int k = 0; k < KEP_K_NCLASS; ++k) fprintf(stderr, " %9.2f", c->lvl_ms[L][k]);
+            fprintf(stderr, "  %6d %6d\n", c->sym.level_ptr[L + 1] - c->sym.level_ptr[L], mx);
+        }
+    }
     while (!c->factors.empty()) kep_factor_destroy(c->factors.back());
     if (c->have_device) {
         cudaSetDevice(c->device);
@@ -1718,7 +1799,8 @@ void kep_destroy(kep_ctx* c) {
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
                         c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1], c->d_rr_l[2], c->d_rr_u, c->d_rr_a, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
-                        c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small, c->d_f0, c->d_resid, c->d_ritems};
+                        c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small, c->d_f0, c->d_resid, c->d_ritems,
+                        c->d_smfronts};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

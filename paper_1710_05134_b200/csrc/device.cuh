@@ -199,6 +199,9 @@ int resid_tile();
 void launch_capture(const DevPlan& P, const int32_t* fronts, int nfronts, double* F0, cudaStream_t st);
 void launch_resid(const DevPlan& P, const StorePlan& T, const int4* items, int nitems, const double* F0, double* out,
                   cudaStream_t st);
+// kernels_small.cu: whole-panel-in-shared-memory partial LDL^T of small fronts
+void launch_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int cap_doubles, int threads,
+                  cudaStream_t st);
 void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st);
 void launch_reset_stats(ShiftStat* st, int batch, cudaStream_t s);
 

@@ -176,7 +176,7 @@ __device__ __forceinline__ void assemble_strip(const DevPlan& P, const int s, co
                     const int fc = P.forder[c] + nd_in[c];
                     AsmKid k;
                     k.F = arena + P.arena_off[c];
-                    k.ldc = ldpad(fc);
+                    k.ldc = ldpad(P.cap[c]);
                     k.ec = fc - mc;
                     k.ndo = nz;
                     k.mc = mc;
@@ -213,7 +213,7 @@ __device__ __forceinline__ void assemble_strip(const DevPlan& P, const int s, co
     }
     __syncthreads();
     if (s_skip) return;
-    const int nd = s_nd, fo = P.forder[s] + nd, ld = ldpad(fo);   // order, leading dimension
+    const int nd = s_nd, fo = P.forder[s] + nd, ld = ldpad(P.cap[s]);   // order, leading dimension
     double* F = arena + P.arena_off[s];
     int clo, chi;
     tri_split(fo, S, xs, clo, chi);
@@ -363,7 +363,7 @@ __device__ __forceinline__ void assemble_strip(const DevPlan& P, const int s, co
         doffs += ndo > 0 ? ndo : 0;
         if (gather && ndo <= 0) continue;
         const int fc = P.forder[c] + nd_in[c];
-        const int ldc = ldpad(fc);
+        const int ldc = ldpad(P.cap[c]);
         const int mc = ndo + P.ncb[c];
         const int ec = fc - mc;
         const double* __restrict__ Fc = arena + P.arena_off[c];
@@ -456,7 +456,7 @@ __device__ __forceinline__ void assemble_front_red(const DevPlan& P, const int32
     }
     __syncthreads();
     if (s_skip) return;
-    const int nd = s_nd, p = P.npiv[s], fo = P.forder[s] + nd, ld = ldpad(fo);   // order, leading dimension
+    const int nd = s_nd, p = P.npiv[s], fo = P.forder[s] + nd, ld = ldpad(P.cap[s]);   // order, leading dimension
     double* F = arena + P.arena_off[s];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAsmRedThreads / 32;
     int clo, chi;
@@ -497,7 +497,7 @@ __device__ __forceinline__ void assemble_front_red(const DevPlan& P, const int32
         const int c = P.child_list[q];
         const int ndo = nd_out[c];
         const int fc = P.forder[c] + nd_in[c];       // child order
-        const int ldc = ldpad(fc);                   // child leading dimension
+        const int ldc = ldpad(P.cap[c]);             // child leading dimension
         const int mc = ndo + P.ncb[c];
         const int ec = fc - mc;
         const double* __restrict__ Fc = arena + P.arena_off[c];
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(kRefThreads) k_factor_ref(DevPlan P, const int
     }
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
     const bool root = (c == 0);
     const double u = P.u;
     const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);

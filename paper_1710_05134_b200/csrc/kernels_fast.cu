@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
     if (P.flag[(size_t)sh * P.nf + s] != FL_OK) return;   // redone by the unblocked kernel (CB updated there)
     const int ndo = P.nd_out[(size_t)sh * P.nf + s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
     const int e = q - ndo;                       // eliminated pivots = K
     if (e <= 0) return;
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(SS_T) k_schur_small(DevPlan P, const int32_t* 
     if (P.flag[(size_t)sh * P.nf + s] != FL_OK) return;
     const int ndo = P.nd_out[(size_t)sh * P.nf + s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
     const int e = q - ndo;
     if (e <= 0 || c <= 0) return;
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];

@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(TH) k_fsp(DevPlan P, const int32_t* __restrict
     if (threadIdx.x == 0) *flag = FL_ACTIVE;
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
     (void)f;
     const bool root = (c == 0);
     const double u = P.u;
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(UT) k_fsu(DevPlan P, const int4* __restrict__ 
     if (K <= 0) return;
     const int nd = P.nd_in[(size_t)sh * P.nf + s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int q = p + nd, ld = ldpad(P.forder[s] + nd);
+    const int q = p + nd, ld = ldpad(P.cap[s]);
     const int i0 = e + 64 * I, j0 = e + 64 * J;
     if (i0 >= q) return;
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
     const int ndo = P.nd_out[(size_t)sh * P.nf + s];
     if (ndo < 0) return;
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
     const int e = q - ndo;
     const int r0 = q + I * LR;
     if (r0 >= f) return;
@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(XPW * 32) k_l21x_prep(DevPlan P, const int32_t
     const int ndo = P.nd_out[(size_t)sh * P.nf + s];
     if (ndo < 0) return;
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
     const int e = q - ndo;
     const double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
     const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
@@ -1008,7 +1008,7 @@ __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restri
     __shared__ int s_fail;
     const int ndo = P.nd_out[(size_t)sh * P.nf + s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(f);
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
     const int e = q - ndo;
     const bool root = c == 0;
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];

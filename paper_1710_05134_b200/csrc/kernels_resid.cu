@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) k_capture(DevPlan P, const int32_t* __res
     const int s = fronts[blockIdx.x];
     const int nd = P.nd_in[s];
     if (nd < 0) return;
-    const int f = P.forder[s] + nd, ld = ldpad(f);
+    const int f = P.forder[s] + nd, ld = ldpad(P.cap[s]);
     const double* src = P.arena + P.arena_off[s];
     double* dst = F0 + P.arena_off[s];
     for (int j = blockIdx.y; j < f; j += gridDim.y)
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(RT) k_resid(DevPlan P, StorePlan T, const int4
     }
     const int c = P.ncb[s];
     const AuxRec A = aux_rec(P, 0, s, P.cap[s] - c);
-    const int ld = ldpad(f);
+    const int ld = ldpad(P.cap[s]);
     const double* F = P.arena + P.arena_off[s];
     const double* G = F0 + P.arena_off[s];
     const int ndo = q - e;

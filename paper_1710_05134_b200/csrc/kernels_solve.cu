@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const in
     const int s = fronts[blockIdx.x];
     const int nd = P.nd_in[s];
     const int p = P.npiv[s], c = P.ncb[s];
-    const int f = P.forder[s] + nd, q = p + nd, ldf = ldpad(f), ld = f;     // ldf: front, ld: stored panel
+    const int f = P.forder[s] + nd, q = p + nd, ldf = ldpad(P.cap[s]), ld = f;     // ldf: front, ld: stored panel
     const int e = q - P.nd_out[s];
     const int flag = P.flag[s];
     const double* F = P.arena + P.arena_off[s];

@@ -14,13 +14,13 @@ import kepgen  # noqa: E402
 from paper_1710_05134_b200 import Kep  # noqa: E402
 
 
-def cached(cfg):
-    path = f"/root/.cache/kep_c{cfg}.npz"
+def cached(cfg, shape=None):
+    path = f"/root/.cache/kep_c{cfg}{'_' + 'x'.join(map(str, shape)) if shape else ''}.npz"
     if os.path.exists(path):
         z = np.load(path)
         return kepgen.Pencil(n=int(z["n"]), colptr=z["colptr"], rowidx=z["rowidx"], a=z["a"], b=z["b"], o=int(z["o"])), \
             float(z["lo"]), float(z["hi"])
-    p = kepgen.config(cfg)
+    p = kepgen.config(cfg, shape=shape)
     lo, hi = kepgen.spectral_bounds(p)
     os.makedirs("/root/.cache", exist_ok=True)
     np.savez(path, n=p.n, colptr=p.colptr, rowidx=p.rowidx, a=p.a, b=p.b, o=p.o, lo=lo, hi=hi)
@@ -30,8 +30,9 @@ def cached(cfg):
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+shape = tuple(int(x) for x in sys.argv[4].split("x")) if len(sys.argv) > 4 else None
 t = time.time()
-p, lo, hi = cached(cfg)
+p, lo, hi = cached(cfg, shape)
 print(f"gen {time.time() - t:.1f}s n={p.n}", flush=True)
 k = Kep.from_pencil(p, max_batch=m, profile=True)
 a = k.analysis()
