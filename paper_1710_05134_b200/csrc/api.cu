@@ -107,6 +107,12 @@ struct kep_ctx {
     double* d_resid = nullptr;
     int4* d_ritems = nullptr;
     std::vector<int64_t> ritem_off, ritem_cnt;
+    // TMA tensor maps of the arena (k_schur_tma): [batch][distinct leading dimensions]
+    CUtensorMap* d_tmaps = nullptr;
+    int32_t* d_tmap_idx = nullptr;
+    int32_t ntmap = 0;
+    bool use_tma = false;
+    std::vector<char> tma_level;                // per level: Schur tiles through k_schur_tma (long K)
     // profiling
     kep_profile prof;
     std::vector<cudaEvent_t> ev_pool;
@@ -219,6 +225,32 @@ kep_status alloc_batch(kep_ctx* c) {
     KEP_CUDA(c, cudaMalloc(&c->d_xscr, sizeof(double) * std::max<int64_t>(c->xstride, 1) * cap));
     KEP_CUDA(c, cudaMalloc(&c->d_pending, 2 * sizeof(int32_t)));
     c->h_stats.resize(cap);
+    // tensor maps: one per (distinct front leading dimension, shift of the batch)
+    cudaFree(c->d_tmaps); c->d_tmaps = nullptr;
+    cudaFree(c->d_tmap_idx); c->d_tmap_idx = nullptr;
+    c->use_tma = false;
+    if (!getenv("KEP_NO_TMA")) {
+        const Symbolic& S = c->sym;
+        std::vector<int> lds;
+        std::vector<int32_t> idx(std::max<int64_t>(S.nf, 1), 0);
+        for (int64_t s = 0; s < S.nf; ++s) lds.push_back(kep::ldpad(S.capacity[s]));
+        std::sort(lds.begin(), lds.end());
+        lds.erase(std::unique(lds.begin(), lds.end()), lds.end());
+        for (int64_t s = 0; s < S.nf; ++s)
+            idx[s] = (int32_t)(std::lower_bound(lds.begin(), lds.end(), kep::ldpad(S.capacity[s])) - lds.begin());
+        std::vector<CUtensorMap> maps((size_t)cap * lds.size());
+        bool ok = !lds.empty();
+        for (int b = 0; b < cap && ok; ++b)
+            for (size_t k = 0; k < lds.size() && ok; ++k)
+                ok = kep::encode_front_tmap(&maps[(size_t)b * lds.size() + k], c->d_arena + (size_t)b * S.arena_doubles,
+                                            S.arena_doubles, lds[k]);
+        if (ok) {
+            KEP_CUDA(c, upload(&c->d_tmaps, maps));
+            KEP_CUDA(c, upload(&c->d_tmap_idx, idx));
+            c->ntmap = (int32_t)lds.size();
+            c->use_tma = true;
+        }
+    }
     return KEP_OK;
 }
 
@@ -421,6 +453,14 @@ kep_status build_lists(kep_ctx* c) {
         mx_u = std::max(mx_u, c->uitem_cnt[L]);
         mx_a = std::max(mx_a, c->raitem_cnt[L]);
         c->small_cnt[L] = (int64_t)small.size() - c->small_off[L];
+    }
+    // TMA-fed Schur tiles where K (the pivots of a front) is long: measured equal to the cp.async
+    // kernel at K >= 128 and slower below (per-CTA barrier/tensor-map setup over few K chunks)
+    c->tma_level.assign(nl, 0);
+    for (int L = 0; L < nl; ++L) {
+        double sp = 0.0, nfr = 0.0;
+        for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) { sp += S.npiv[S.level_fronts[k]]; nfr += 1.0; }
+        c->tma_level[L] = nfr > 0.0 && sp / nfr >= 128.0;
     }
     for (int L = 0; L < nl; ++L)
         for (int64_t k = c->fast_off[L]; k < c->fast_off[L] + c->fast_cnt[L]; ++k) {
@@ -632,6 +672,9 @@ DevPlan make_plan(kep_ctx* c) {
     P.xstride = c->xstride;
     P.xoff = c->d_xoff;
     P.debug = getenv("KEP_DEBUG") ? 1 : 0;
+    P.tmaps = c->d_tmaps;
+    P.tmap_idx = c->d_tmap_idx;
+    P.ntmap = c->ntmap;
     return P;
 }
 
@@ -838,7 +881,8 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             if (keep) kep::launch_store(P, keep->plan(), c->d_level_fronts + b, nfl, c->stream);
             if (c->item_cnt[L] || c->small_cnt[L]) {
                 mark(KEP_K_SCHUR, true);
-                kep::launch_schur(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
+                if (c->use_tma && c->tma_level[L]) kep::launch_schur_tma(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
+                else kep::launch_schur(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
                 kep::launch_schur_small(P, c->d_small + c->small_off[L], (int)c->small_cnt[L], m, c->stream);
                 mark(KEP_K_SCHUR, false);
                 c->prof.launches[KEP_K_SCHUR] += (c->item_cnt[L] ? 1 : 0) + (c->small_cnt[L] ? 1 : 0);
@@ -1800,7 +1844,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
                         c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1], c->d_rr_l[2], c->d_rr_u, c->d_rr_a, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
                         c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small, c->d_f0, c->d_resid, c->d_ritems,
-                        c->d_smfronts};
+                        c->d_smfronts, c->d_tmaps, c->d_tmap_idx};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -1,6 +1,7 @@
 // device.cuh — device-side plan, per-shift state and shared helpers.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace kep {
@@ -62,6 +63,11 @@ struct DevPlan {
     int64_t xstride;
     const int64_t* xoff;         // [nf] offset in the level's X scratch (k_l21<2> fronts)
     int32_t debug;               // KEP_DEBUG set: diagnostic printf in rare paths
+    // TMA: one 2-D tensor map (x = ld doubles, y = arena rows of ld) per distinct leading dimension
+    // and shift of the batch; fronts start at multiples of their ld (plan_memory)
+    const CUtensorMap* tmaps;    // [batch][ntmap]
+    const int32_t* tmap_idx;     // [nf] index of the front's leading dimension
+    int32_t ntmap;
 };
 
 // pivot kinds recorded per eliminated position
@@ -190,6 +196,10 @@ void launch_l21x_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int 
 void launch_check(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 int front_nb_for(int qmax, int64_t nblocks = 0);   // block width (0: too large, use the reference kernel)
 void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
+void launch_schur_tma(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);
+// host: encode the 2-D tensor map of one (arena base, leading dimension) pair (TMA box 16 x 64 doubles,
+// 128-byte swizzle); false if the driver entry point is unavailable
+bool encode_front_tmap(CUtensorMap* out, double* arena_base, int64_t arena_doubles, int ld);
 void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
 bool schur_small_ok(int c, int qcap);     // front handled by k_schur_small
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,

@@ -10,6 +10,8 @@
 #include <climits>
 #include <cstdint>
 
+#include <cudaTypedefs.h>
+
 #include "device.cuh"
 
 namespace kep {
@@ -122,6 +124,138 @@ __global__ void __launch_bounds__(SCH_T) k_schur(DevPlan P, const int4* __restri
             }
 }
 
+// ---------------------------------------------------------------- k_schur_tma
+// The same tile computation fed by TMA (cp.async.bulk.tensor, SASS UTMALDG): per K
+// chunk of 16 pivots, one elected thread issues two 16 x 64 boxes (the G rows of the
+// tile's CB rows and of its CB columns) from the front's tensor map into a 128-byte
+// swizzled stage and arms the stage's "full" mbarrier with the byte count; the four
+// warps wait on it, run the DMMA k-steps and arrive on the stage's "empty" mbarrier;
+// the producer refills a stage once it is empty.  KST stages in flight, no CTA-wide
+// barrier in the K loop.  Columns t >= e of the last chunk (other data of the front)
+// are masked on the B fragments together with the D-sign flip.
+constexpr int KST = 3;                        // pipeline stages (48 KB: 4 CTAs per SM)
+constexpr int TBOX = ST * KC;                 // doubles per box (64 rows x 16 pivots, 8 KB)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)) : "memory");
+}
+// element (row, t) of a 64 x 16 box stored with the 128-byte swizzle: 16-byte chunk (t / 2) ^ (row % 8)
+__device__ __forceinline__ int swz(int row, int t) { return row * KC + ((((t >> 1) ^ (row & 7)) << 1) | (t & 1)); }
+
+__global__ void __launch_bounds__(SCH_T, 4) k_schur_tma(DevPlan P, const int4* __restrict__ items) {
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    const unsigned pad = (1024u - (smem_u32(tsm) & 1023u)) & 1023u;  // the 128-byte swizzle atom is 1 KB
+    double* As = reinterpret_cast<double*>(tsm + pad);            // [KST][64][16] swizzled
+    double* Bs = As + KST * TBOX;                                 // [KST][64][16]
+    __shared__ __align__(8) uint64_t full[KST], empty[KST];
+    const int4 it = items[blockIdx.x];
+    const int s = it.x, I = it.y, J = it.z;
+    const int sh = blockIdx.y;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    if (nd < 0) return;
+    if (P.flag[(size_t)sh * P.nf + s] != FL_OK) return;
+    const int ndo = P.nd_out[(size_t)sh * P.nf + s];
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
+    const int e = q - ndo;
+    if (e <= 0) return;
+    const int r0 = q + I * ST, c0 = q + J * ST;
+    if (r0 >= f) return;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, tg = lane & 3;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const CUtensorMap* map = P.tmaps + (size_t)sh * P.ntmap + P.tmap_idx[s];
+    const int ybase = (int)(P.arena_off[s] / ld);                 // the front starts at a multiple of ld
+    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
+    const int nk = (e + KC - 1) / KC;
+    if (tid == 0) {
+        for (int k = 0; k < KST; ++k) { mbar_init(&full[k], 1); mbar_init(&empty[k], SCH_T / 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(map) : "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int kc) {
+        const int st = kc % KST;
+        mbar_expect_tx(&full[st], 2 * TBOX * sizeof(double));
+        tma_load_2d(As + st * TBOX, map, kc * KC, ybase + r0, &full[st]);
+        tma_load_2d(Bs + st * TBOX, map, kc * KC, ybase + c0, &full[st]);
+    };
+    if (tid == 0)
+        for (int kc = 0; kc < KST && kc < nk; ++kc) issue(kc);
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int kc = 0; kc < nk; ++kc) {
+        const int st = kc % KST;
+        // masks of this chunk's pivots (t = kc KC + 4 k4 + tg): bit k4 keep (t < e), bit 4 + k4 sign of D
+        unsigned msk = 0;
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+            const int t = kc * KC + 4 * k4 + tg;
+            if (t < e) msk |= (1u << k4) | (A.sgn[t] < 0.0 ? (16u << k4) : 0u);
+        }
+        mbar_wait(&full[st], (unsigned)((kc / KST) & 1));
+        const double* as = As + st * TBOX;
+        const double* bs = Bs + st * TBOX;
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+            double a[4], b[4];
+            const long long keep = ((msk >> k4) & 1u) ? -1ll : 0ll;
+            const long long sgn = (long long)((unsigned long long)((msk >> (4 + k4)) & 1u) << 63);
+#pragma unroll
+            for (int mb = 0; mb < 4; ++mb) a[mb] = as[swz(wm + 8 * mb + g, 4 * k4 + tg)];
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb)
+                b[nb] = __longlong_as_double((__double_as_longlong(bs[swz(wn + 8 * nb + g, 4 * k4 + tg)]) & keep) ^ sgn);
+#pragma unroll
+            for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb], a[mb], b[nb]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (tid == 0 && kc + KST < nk) {                        // refill this stage once every warp is done
+            mbar_wait(&empty[st], (unsigned)((kc / KST) & 1));
+            issue(kc + KST);
+        }
+    }
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = r0 + wm + 8 * mb + g;
+                const int j = c0 + wn + 8 * nb + 2 * tg + h;
+                double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+                if (i < f && j < f && i >= j) atomicAdd(&F[i + (size_t)j * ld], -acc[mb][nb][h]);
+            }
+}
+
 // Small fronts (c <= 256, FS block <= 48): one CTA per front, the CB's G rows
 // staged in shared memory once, every 32 x 32 lower tile of the CB computed from
 // them (DMMA), RED epilogue.  Avoids the per-tile setup and the repeated operand
@@ -209,9 +343,39 @@ void launch_schur(const DevPlan& P, const int4* items, int nitems, int batch, cu
     k_schur<<<dim3(nitems, batch), SCH_T, 0, st>>>(P, items);
 }
 
+void launch_schur_tma(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
+    if (nitems <= 0) return;
+    const size_t smem = 2 * KST * TBOX * sizeof(double) + 1024;     // + alignment slack for the 1 KB swizzle atom
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) cudaFuncSetAttribute(k_schur_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_schur_tma<<<dim3(nitems, batch), SCH_T, smem, st>>>(P, items);
+}
+
 }  // namespace kep
 
 namespace kep {
+bool encode_front_tmap(CUtensorMap* out, double* base, int64_t arena_doubles, int ld) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !ptr) {
+            cudaGetLastError();
+            return false;
+        }
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)(arena_doubles / ld)};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)ST};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool schur_small_ok(int c, int qcap) { return c > 0 && c <= SS_C && qcap <= SS_K; }
 
 void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {

@@ -44,27 +44,33 @@ void plan_memory(Symbolic& S, int slack) {
     const int64_t nf = S.nf;
     S.capacity.assign(nf, 0);
     S.arena_off.assign(nf, 0);
-    std::vector<int64_t> need(nf);
+    std::vector<int64_t> need(nf), align(nf);
     for (int64_t s = 0; s < nf; ++s) {
         int64_t cap = (int64_t)S.forder[s] + slack;
         S.capacity[s] = (int32_t)cap;
-        const int64_t ldc = (cap + 1) & ~int64_t(1);  // fronts use an even leading dimension (ldpad)
-        need[s] = ((ldc * cap + 31) / 32) * 32;       // 256-byte aligned blocks
+        const int64_t ldc = (cap + 1) & ~int64_t(1);  // fronts use an even leading dimension ldpad(capacity)
+        need[s] = ldc * cap;
+        // a front starts at a multiple of its leading dimension, so one 2-D TMA tensor map per distinct
+        // leading dimension (rows of ld doubles over the whole arena) addresses every front with it
+        align[s] = ldc;
     }
     std::map<int64_t, int64_t> freel;                 // offset -> size
     int64_t top = 0;
-    auto alloc = [&](int64_t sz) -> int64_t {
+    auto alloc = [&](int64_t sz, int64_t al) -> int64_t {
         for (auto it = freel.begin(); it != freel.end(); ++it) {
-            if (it->second >= sz) {
-                int64_t off = it->first, rem = it->second - sz;
+            const int64_t off = it->first, end = it->first + it->second;
+            const int64_t a = (off + al - 1) / al * al;
+            if (a + sz <= end) {
                 freel.erase(it);
-                if (rem > 0) freel[off + sz] = rem;
-                return off;
+                if (a > off) freel[off] = a - off;
+                if (end > a + sz) freel[a + sz] = end - (a + sz);
+                return a;
             }
         }
-        int64_t off = top;
-        top += sz;
-        return off;
+        const int64_t a = (top + al - 1) / al * al;
+        if (a > top) freel[top] = a - top;            // alignment gap: reusable
+        top = a + sz;
+        return a;
     };
     auto release = [&](int64_t off, int64_t sz) {
         auto it = freel.emplace(off, sz).first;
@@ -91,7 +97,7 @@ void plan_memory(Symbolic& S, int slack) {
     for (int64_t L = 0; L < nl; ++L) {
         for (int32_t k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
             int32_t s = S.level_fronts[k];
-            S.arena_off[s] = alloc(need[s]);
+            S.arena_off[s] = alloc(need[s], align[s]);
         }
         peak = std::max(peak, top);
         for (int32_t k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
