@@ -19,7 +19,7 @@ METIS = "/usr/local/cuda/lib64/libcusolver_metis_static.a"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
            "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-SOURCES_CU = ["api.cu", "kernels.cu", "kernels_front.cu", "kernels_fast.cu", "kernels_solve.cu", "kth.cu", "kernels_resid.cu", "kernels_small.cu"]
+SOURCES_CU = ["api.cu", "kernels.cu", "kernels_front.cu", "kernels_fast.cu", "kernels_solve.cu", "kth.cu", "kernels_resid.cu", "kernels_small.cu", "kernels_big.cu"]
 SOURCES_CPP = ["symbolic.cpp", "tridiag.cpp"]
 
 

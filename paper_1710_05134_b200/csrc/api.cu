@@ -97,6 +97,16 @@ struct kep_ctx {
     // k_small (whole FS panel in shared memory): per level list offsets, shared-memory cap, threads
     int32_t* d_smfronts = nullptr;
     struct SmGroup { int64_t off, cnt; int cap, th; };
+    // k_bigp/k_bigu/k_bigfin (multi-CTA partial LDL^T of the few large fronts of a level): per level the
+    // groups (front, shift) shift-major for big_m shifts, their scratch offsets, the largest FS block
+    int big_m = 0;                              // shifts the big-front groups are planned for
+    std::vector<int64_t> big_goff, big_nf;      // per level: first group, big fronts
+    std::vector<int> big_qmax;
+    int2* d_big_groups = nullptr;
+    int64_t* d_big_scroff = nullptr;
+    double* d_big_scr = nullptr;
+    int* d_big_state = nullptr;
+    unsigned* d_big_bars = nullptr;
     std::vector<std::vector<SmGroup>> sm_groups;    // per level: size classes of the k_small fronts
     int32_t* d_small = nullptr;                  // fronts whose Schur update runs in k_schur_small
     std::vector<int> level_qmax;                // per level: max p + slack over its fast fronts
@@ -151,6 +161,8 @@ namespace {
 thread_local std::string g_err;
 constexpr int kReruns = 2;      // fast-path reruns per level before the unblocked fallback
 constexpr int kSmallDelay = 8;  // k_small eligibility: the panel with this many delayed-in columns fits kSmallCap
+constexpr int kBigQ = 2048;        // big fronts: FS capacity at least this (c4 root, 1216: faster on k_fsp) ...
+constexpr int kBigGroups = 74;      // ... on levels with at most this many (front, shift) groups (>= 2 SMs each)
 constexpr int kSmallMaxPiv = 16;   // k_small: fronts with at most this many own pivots
 constexpr int kSmallPlan = 2;   // k_small size class: planned delayed-in columns (more, beyond the class cap: k_factor_ref)
 constexpr int64_t kSmallCap = 24 * 1024;   // k_small: FS panel budget in doubles (192 KB of shared memory)
@@ -254,6 +266,8 @@ kep_status alloc_batch(kep_ctx* c) {
     return KEP_OK;
 }
 
+int nl_all(const Symbolic& S) { return (int)S.level_ptr.size() - 1; }
+
 // Split every level into fronts for the blocked panel kernel (+ DMMA Schur
 // tiles) and fronts for the reference kernel; build the Schur work items.
 kep_status build_lists(kep_ctx* c) {
@@ -267,9 +281,29 @@ kep_status build_lists(kep_ctx* c) {
         // (measured at c4: faster than the k_fsp/k_l21/k_check path up to ~16 pivots, slower beyond)
         return use_small && S.ncb[s] > 0 && S.npiv[s] <= kSmallMaxPiv && (int64_t)S.forder[s] * qq <= kSmallCap;
     };
+    // big fronts: levels with few large FS blocks (all SMs on them, kernels_big.cu)
+    if (c->big_m <= 0) c->big_m = std::max(1, c->opts.max_batch);
+    std::vector<char> big(std::max<int64_t>(S.nf, 1), 0);
+    int bigq = kBigQ;
+    if (const char* e = getenv("KEP_BIG_Q")) bigq = std::max(2, atoi(e));      // testing: route smaller fronts
+    if (c->opts.kernel_variant == 0 && !getenv("KEP_NO_BIG")) {
+        for (int L = 0; L + 1 < (int)S.level_ptr.size(); ++L) {
+            int nb = 0;
+            for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k)
+                nb += S.capacity[S.level_fronts[k]] - S.ncb[S.level_fronts[k]] >= bigq;
+            if (nb == 0 || nb * c->big_m > kBigGroups) continue;
+            for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k)
+                if (S.capacity[S.level_fronts[k]] - S.ncb[S.level_fronts[k]] >= bigq) big[S.level_fronts[k]] = 1;
+        }
+    }
+    auto is_big = [&](int s) { return big[s] != 0; };
     auto is_fast = [&](int s) {
-        return c->opts.kernel_variant == 0 && !is_small(s) && kep::front_nb_for(S.capacity[s] - S.ncb[s]) > 0;
+        return c->opts.kernel_variant == 0 && !is_small(s) && !is_big(s) && kep::front_nb_for(S.capacity[s] - S.ncb[s]) > 0;
     };
+    std::vector<int2> bgroups;
+    std::vector<int64_t> bscr;
+    int64_t bscr_acc = 0, bscr_max = 0;
+    c->big_goff.assign(nl_all(S), 0); c->big_nf.assign(nl_all(S), 0); c->big_qmax.assign(nl_all(S), 0);
     const int nl = (int)S.level_ptr.size() - 1;
     std::vector<int32_t> smf;
     c->sm_groups.assign(nl, {});
@@ -351,10 +385,34 @@ kep_status build_lists(kep_ctx* c) {
                 if (g.cnt) c->sm_groups[L].push_back(g);
             }
         }
+        {   // big-front groups of this level: shift-major, so the first nbig * m serve a batch of m
+            std::vector<int> bl;
+            for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k)
+                if (is_big(S.level_fronts[k])) bl.push_back(S.level_fronts[k]);
+            c->big_goff[L] = (int64_t)bgroups.size();
+            c->big_nf[L] = (int64_t)bl.size();
+            int64_t acc = 0;
+            for (int sh = 0; sh < c->big_m; ++sh)
+                for (int s : bl) {
+                    bgroups.push_back(make_int2(s, sh));
+                    bscr.push_back(acc);
+                    acc += (int64_t)kep::big_scratch_doubles(S.capacity[s], kBigGroups);
+                    c->big_qmax[L] = std::max(c->big_qmax[L], S.capacity[s] - S.ncb[s]);
+                }
+            bscr_max = std::max(bscr_max, acc);
+            (void)bscr_acc;
+        }
         // tile lists in the level's front order
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
             const int s = S.level_fronts[k];
             const int qcap = S.capacity[s] - S.ncb[s];            // p + slack
+            if (is_big(s)) {                                       // k_bigp..k_bigfin, then the Schur tiles
+                const int nt = (S.ncb[s] + 63) / 64;
+                for (int I = 0; I < nt; ++I)
+                    for (int J = 0; J <= I; ++J) items.push_back(make_int4(s, I, J, 0));
+                c->item_flops[L] += (double)S.npiv[s] * (double)S.ncb[s] * (double)(S.ncb[s] + 1);
+                continue;
+            }
             if (is_small(s)) {                                     // k_small, then the Schur tiles
                 const int qq = S.npiv[s] + kSmallDelay;
                 if (kep::schur_small_ok(S.ncb[s], qq)) {
@@ -532,6 +590,18 @@ kep_status build_lists(kep_ctx* c) {
     KEP_CUDA(c, upload(&c->d_goff, goff));
     KEP_CUDA(c, upload(&c->d_lists, lists));
     KEP_CUDA(c, upload(&c->d_items, items));
+    {
+        void* old[] = {c->d_big_groups, c->d_big_scroff, c->d_big_scr, c->d_big_state, c->d_big_bars};
+        for (void* q : old) cudaFree(q);
+        c->d_big_groups = nullptr; c->d_big_scroff = nullptr; c->d_big_scr = nullptr;
+        c->d_big_state = nullptr; c->d_big_bars = nullptr;
+        KEP_CUDA(c, upload(&c->d_big_groups, bgroups));
+        KEP_CUDA(c, upload(&c->d_big_scroff, bscr));
+        KEP_CUDA(c, cudaMalloc(&c->d_big_scr, std::max<int64_t>(bscr_max, 1) * sizeof(double)));
+        const size_t ng = std::max<size_t>(bgroups.size(), 1);
+        KEP_CUDA(c, cudaMalloc(&c->d_big_state, ng * 16 * sizeof(int)));
+        KEP_CUDA(c, cudaMalloc(&c->d_big_bars, ng * sizeof(unsigned)));
+    }
     return KEP_OK;
 }
 
@@ -608,7 +678,15 @@ kep_status upload_plan(kep_ctx* c, const int64_t* colptr, const int32_t* rowidx)
     KEP_CUDA(c, cudaMalloc(&c->d_b, std::max<int64_t>(S.nnz, 1) * sizeof(double)));
     kep_status r = build_lists(c);
     if (r != KEP_OK) return r;
-    return alloc_batch(c);
+    r = alloc_batch(c);
+    if (r != KEP_OK) return r;
+    if (c->batch_cap < c->big_m) {                    // big-front levels are chosen for the batch that fits
+        c->big_m = c->batch_cap;
+        r = build_lists(c);
+        if (r != KEP_OK) return r;
+        r = alloc_batch(c);
+    }
+    return r;
 }
 
 // after a slack overflow: larger slack, new plan, re-upload the plan arrays that changed
@@ -762,6 +840,16 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             else kep::launch_assemble(P, c->d_aitems + c->aitem_off[L], (int)c->aitem_cnt[L], m, false, c->stream);
             mark(KEP_K_ASSEMBLE, false);
             if (resid) kep::launch_capture(P, c->d_level_fronts + b, nfl, c->d_f0, c->stream);
+            if (c->big_nf[L] > 0) {                          // large fronts, all SMs (kernels_big.cu)
+                const int ng = (int)(c->big_nf[L] * m);
+                const int ncta = std::max(1, std::min(148 / ng, kBigGroups));
+                mark(KEP_K_PANEL, true);
+                kep::launch_bigfront(P, c->d_big_groups + c->big_goff[L], ng, ncta, c->d_big_scroff + c->big_goff[L],
+                                     c->d_big_scr, c->d_big_state + 16 * c->big_goff[L],
+                                     c->d_big_bars + c->big_goff[L], c->big_qmax[L], c->stream);
+                mark(KEP_K_PANEL, false);
+                c->prof.launches[KEP_K_PANEL] += 2 + 2 * ((c->big_qmax[L] + kep::big_block() - 2) / (kep::big_block() - 1) + 1);
+            }
             for (const auto& g : c->sm_groups[L]) {         // whole-panel fronts; overflow -> unblocked kernel
                 mark(KEP_K_PANEL, true);
                 kep::launch_small(P, c->d_smfronts + g.off, (int)g.cnt, m, g.cap, g.th, c->stream);
@@ -1844,7 +1932,8 @@ void kep_destroy(kep_ctx* c) {
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
                         c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1], c->d_rr_l[2], c->d_rr_u, c->d_rr_a, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
                         c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small, c->d_f0, c->d_resid, c->d_ritems,
-                        c->d_smfronts, c->d_tmaps, c->d_tmap_idx};
+                        c->d_smfronts, c->d_tmaps, c->d_tmap_idx, c->d_big_groups, c->d_big_scroff, c->d_big_scr,
+                        c->d_big_state, c->d_big_bars};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

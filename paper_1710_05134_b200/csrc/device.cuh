@@ -212,6 +212,11 @@ void launch_resid(const DevPlan& P, const StorePlan& T, const int4* items, int n
 // kernels_small.cu: whole-panel-in-shared-memory partial LDL^T of small fronts
 void launch_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int cap_doubles, int threads,
                   cudaStream_t st);
+// kernels_big.cu: multi-CTA partial LDL^T of the large fronts of the top levels
+int big_block();
+size_t big_scratch_doubles(int cap, int ncta);
+void launch_bigfront(const DevPlan& P, const int2* groups, int ngroups, int ncta, const int64_t* scroff, double* scr,
+                     int* state, unsigned* bars, int qmax, cudaStream_t st);
 void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st);
 void launch_reset_stats(ShiftStat* st, int batch, cudaStream_t s);
 

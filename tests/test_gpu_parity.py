@@ -201,3 +201,34 @@ def test_twin_c5_geometry_full_size():
     nus, st = k.inertia_many(sig)
     assert np.all(st == KEP_OK)
     assert np.array_equal(nus, oracle.nu_twin(q.meta["twin"], sig, w))
+
+
+@pytest.mark.parametrize("u", [0.01, 0.5])
+def test_big_front_path_c1_c2(monkeypatch, u):
+    """kernels_big.cu (multi-CTA panel of the top-level fronts) routed onto the c1 / c2 top levels
+    (KEP_BIG_Q lowers its FS threshold): nu equals LAPACK eigh at every certified shift (c1, with
+    u = 0.5 many delays) and the stored factor reconstructs A - sigma B (front-local residual bound)."""
+    monkeypatch.setenv("KEP_BIG_Q", "48")
+    p = kepgen.config(1)
+    A, B = p.dense("a"), p.dense("b")
+    w = oracle.eigvals_pencil(A, B)
+    sig = kepgen.uniform_shifts(w[0], w[-1], 32)
+    sig = sig[_certified(w, sig)]
+    k = Kep.from_pencil(p, pivot_u=u)
+    k.set_values(p.a, p.b)
+    nus, st = k.inertia_many(sig)
+    assert np.all(st == KEP_OK)
+    assert np.array_equal(nus, oracle.nu_eig(A, B, sig, eigvals=w))
+    for s in sig[::8]:
+        bound, _ = k.factor_residual(s)
+        assert bound <= 1e-10 * np.linalg.norm(A - s * B)
+    g = json.load(open(os.path.join(GOLD, "c2_nu.json")))
+    p2 = kepgen.config(2)
+    k2 = Kep.from_pencil(p2, pivot_u=u)
+    k2.set_values(p2.a, p2.b)
+    s2 = np.array([x["sigma"] for x in g["shifts"]])
+    nus2, st2 = k2.inertia_many(s2)
+    assert np.all(st2 == KEP_OK)
+    for x, v in zip(g["shifts"], nus2):
+        if x["certified"]:
+            assert v == x["nu"]
