@@ -142,16 +142,19 @@ struct kep_factorization {
     int32_t* lab = nullptr;
     double *d = nullptr, *ds = nullptr;
     int32_t* kind = nullptr;
+    int32_t* perm = nullptr;
     int4* hdr = nullptr;
-    int64_t *poff = nullptr, *loff = nullptr, *qoff = nullptr;
-    std::vector<int64_t> h_poff, h_loff, h_qoff;
+    int64_t *poff = nullptr, *loff = nullptr, *qoff = nullptr, *yoff = nullptr;
+    double *upd = nullptr, *ybuf = nullptr;                 // solve scratch (update vectors, big fronts' vectors)
+    std::vector<int64_t> h_poff, h_loff, h_qoff, h_yoff;
     std::vector<int> level_fmax;                 // per level: max front capacity (shared memory of the solves)
     double *xw = nullptr, *bw = nullptr;         // work vectors (n)
     int64_t panel_doubles = 0, lab_ints = 0, q_entries = 0;
     kep::StorePlan plan() const {
         kep::StorePlan T;
         T.panel = panel; T.poff = poff; T.lab = lab; T.loff = loff;
-        T.d = d; T.ds = ds; T.kind = kind; T.qoff = qoff; T.hdr = hdr;
+        T.d = d; T.ds = ds; T.kind = kind; T.perm = perm; T.qoff = qoff; T.hdr = hdr;
+        T.upd = upd; T.ybuf = ybuf; T.yoff = yoff;
         return T;
     }
 };
@@ -757,10 +760,12 @@ DevPlan make_plan(kep_ctx* c) {
 }
 
 void free_store(kep_factorization* k) {
-    void* ptrs[] = {k->panel, k->lab, k->d, k->ds, k->kind, k->hdr, k->poff, k->loff, k->qoff};
+    void* ptrs[] = {k->panel, k->lab, k->d, k->ds, k->kind, k->perm, k->hdr, k->poff, k->loff, k->qoff, k->yoff,
+                    k->upd, k->ybuf};
     for (void* q : ptrs) cudaFree(q);
-    k->panel = nullptr; k->lab = nullptr; k->d = nullptr; k->ds = nullptr; k->kind = nullptr;
-    k->hdr = nullptr; k->poff = nullptr; k->loff = nullptr; k->qoff = nullptr;
+    k->panel = nullptr; k->lab = nullptr; k->d = nullptr; k->ds = nullptr; k->kind = nullptr; k->perm = nullptr;
+    k->hdr = nullptr; k->poff = nullptr; k->loff = nullptr; k->qoff = nullptr; k->yoff = nullptr;
+    k->upd = nullptr; k->ybuf = nullptr;
 }
 
 // (Re)allocate the factor store for the current memory plan (capacities).
@@ -780,7 +785,17 @@ kep_status prepare_store(kep_ctx* c, kep_factorization* k) {
     KEP_CUDA(c, cudaMalloc(&k->d, std::max<int64_t>(qo, 1) * sizeof(double)));
     KEP_CUDA(c, cudaMalloc(&k->ds, std::max<int64_t>(qo, 1) * sizeof(double)));
     KEP_CUDA(c, cudaMalloc(&k->kind, std::max<int64_t>(qo, 1) * sizeof(int32_t)));
+    KEP_CUDA(c, cudaMalloc(&k->perm, std::max<int64_t>(qo, 1) * sizeof(int32_t)));
+    KEP_CUDA(c, cudaMalloc(&k->upd, std::max<int64_t>(lo, 1) * sizeof(double)));
     KEP_CUDA(c, cudaMalloc(&k->hdr, std::max<int64_t>(S.nf, 1) * sizeof(int4)));
+    {   // fronts beyond the shared-memory solve vectors: global front vectors (2 f doubles each)
+        k->h_yoff.assign(std::max<int64_t>(S.nf, 1), -1);
+        int64_t yo = 0;
+        for (int64_t s = 0; s < S.nf; ++s)
+            if (S.capacity[s] > kep::solve_max_front()) { k->h_yoff[s] = yo; yo += 2 * (int64_t)S.capacity[s]; }
+        KEP_CUDA(c, cudaMalloc(&k->ybuf, std::max<int64_t>(yo, 1) * sizeof(double)));
+        KEP_CUDA(c, upload(&k->yoff, k->h_yoff));
+    }
     KEP_CUDA(c, upload(&k->poff, k->h_poff));
     KEP_CUDA(c, upload(&k->loff, k->h_loff));
     KEP_CUDA(c, upload(&k->qoff, k->h_qoff));
@@ -1344,13 +1359,11 @@ kep_status kep_solve_dev(const kep_factorization* k, const double* b_dev, double
     KEP_CUDA(c, cudaSetDevice(c->device));
     const Symbolic& S = c->sym;
     const int nl = (int)S.level_ptr.size() - 1;
-    for (int L = 0; L < nl; ++L)
-        if (k->level_fmax[L] > kep::solve_max_front())
-            return fail(c, KEP_EINVAL, "front too large for the solve kernels");
     kep::launch_gather(b_dev, c->d_perm, k->xw, S.n, c->stream);          // to elimination positions
     const kep::StorePlan T = k->plan();
+    const DevPlan P = make_plan(c);
     for (int L = 0; L < nl; ++L)
-        kep::launch_fwd(T, c->d_level_fronts + S.level_ptr[L], S.level_ptr[L + 1] - S.level_ptr[L], k->level_fmax[L],
+        kep::launch_fwd(P, T, c->d_level_fronts + S.level_ptr[L], S.level_ptr[L + 1] - S.level_ptr[L], k->level_fmax[L],
                         k->xw, c->stream);
     for (int L = nl - 1; L >= 0; --L)
         kep::launch_bwd(T, c->d_level_fronts + S.level_ptr[L], S.level_ptr[L + 1] - S.level_ptr[L], k->level_fmax[L],

@@ -150,8 +150,14 @@ struct StorePlan {
     double* d;
     double* ds;
     int32_t* kind;
+    int32_t* perm;               // [qoff] local pivot permutation of the FS positions (k_fwd's extend-add)
     const int64_t* qoff;
     int4* hdr;
+    // solve scratch: per front the update vector passed to the parent (f - e rows, at uoff = loff)
+    // and, for fronts too large for shared memory, the front vector itself (at yoff, -1 otherwise)
+    double* upd;
+    double* ybuf;
+    const int64_t* yoff;
 };
 
 // Launchers (kernels.cu, kernels_front.cu, kernels_fast.cu, kernels_solve.cu)
@@ -166,9 +172,10 @@ bool fs_uses_gls(int qmax);                 // the level's block columns live in
 int fs_rows_pad(int qmax);
 size_t fs_gls_doubles(int nb, int RS);
 void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, cudaStream_t st);
-void launch_fwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
+void launch_fwd(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x,
+                cudaStream_t st);
 void launch_bwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
-int solve_max_front();
+int solve_max_front();       // largest front whose solve vector lives in shared memory (larger: global scratch)
 // kth.cu: Lanczos building blocks
 void launch_spmv2(const int64_t* rp, const int32_t* ci, const double* va, const double* vb, const double* x, double* ya,
                   double* yb, int64_t n, cudaStream_t st);

@@ -4,15 +4,19 @@
 // kep_factor keeps, per front s, the panel of its eliminated columns
 // (f_s x e_s, column-major, ld = f_s; unit lower L, zero at the in-pair entry
 // of a 2x2 block), the labels of its rows (elimination positions of the
-// variables: FS positions after pivoting, then the CB rows) and D.  With
-// S = P Q (A - sigma B) Q^T P^T = L D L^T  (Alg. 1' line 3), a
-// solve S y = b is
-//   forward  (postorder levels):  y_e = L11^-1 b_e per front, CB/delayed rows
-//                                 receive -L21 y_e (scatter-add to the parent side),
-//            then z_e = D^-1 y_e;
-//   backward (reverse levels):    x_e = L11^-T (z_e - L21^T x_rest).
+// variables: FS positions after pivoting, then the CB rows), the local pivot
+// permutation and D.  With S = P Q (A - sigma B) Q^T P^T = L D L^T (Alg. 1'
+// line 3), a solve S y = b is
+//   forward  (postorder levels): the front vector is b on the front's own
+//            pivots plus its children's update vectors, extend-added in child
+//            order (the vector analogue of the assembly: deterministic, no
+//            atomics); y_e = L11^-1 y_e, the delayed and CB rows get -L21 y_e
+//            and become this front's update vector; z_e = D^-1 y_e;
+//   backward (reverse levels):   x_e = L11^-T (z_e - L21^T x_rest).
+// Fronts larger than shared memory allows keep their vector in global scratch.
 // These are the shift-and-invert solves of stage 3 (Alg. 3)
 // and of the stage-1 B-solves.
+#include <algorithm>
 #include <cstdint>
 
 #include "device.cuh"
@@ -53,6 +57,7 @@ __global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const in
     if (threadIdx.x == 0) T.hdr[s] = make_int4(e, f, q, flag);
     for (int i = threadIdx.x; i < f; i += ST_T)
         lab[i] = i < q ? A.label[A.perm[i]] : P.cb_rows[P.cb_ptr[s] + (i - q)];
+    for (int i = threadIdx.x; i < q; i += ST_T) T.perm[qo + i] = A.perm[i];
     for (int t = threadIdx.x; t < e; t += ST_T) {
         T.d[qo + t] = A.d[t];
         T.ds[qo + t] = A.ds[t];
@@ -90,16 +95,40 @@ __global__ void __launch_bounds__(ST_T) k_store(DevPlan P, StorePlan T, const in
     }
 }
 
-// forward elimination and D^-1 for the fronts of one level; x in elimination positions
-__global__ void __launch_bounds__(ST_T) k_fwd(StorePlan T, const int32_t* __restrict__ fronts, double* __restrict__ x) {
-    extern __shared__ double y[];
+// forward elimination and D^-1 for the fronts of one level; x in elimination positions (b on
+// entry for every variable, z = D^-1 L^-1 P b for the eliminated ones on exit)
+__global__ void __launch_bounds__(ST_T) k_fwd(DevPlan P, StorePlan T, const int32_t* __restrict__ fronts,
+                                              double* __restrict__ x) {
+    extern __shared__ double ysm[];
     const int s = fronts[blockIdx.x];
     const int4 h = T.hdr[s];
-    const int e = h.x, f = h.y;
+    const int e = h.x, f = h.y, q = h.z;
+    const int p = P.npiv[s], nd = q - p;
     const double* L = T.panel + T.poff[s];
     const int* lab = T.lab + T.loff[s];
     const int64_t qo = T.qoff[s];
-    for (int i = threadIdx.x; i < f; i += ST_T) y[i] = i < e ? x[lab[i]] : 0.0;
+    double* yo = T.yoff[s] >= 0 ? T.ybuf + T.yoff[s] : ysm;            // front vector, original local order
+    double* y = yo + f;                                                  // pivoted order
+    for (int i = threadIdx.x; i < f; i += ST_T) yo[i] = i < p ? x[P.piv_first[s] + i] : 0.0;
+    __syncthreads();
+    // extend-add of the children's update vectors (children in order; rows of one child are distinct)
+    int dof = 0;
+    for (int k = P.child_ptr[s]; k < P.child_ptr[s + 1]; ++k) {
+        const int c = P.child_list[k];
+        const int4 hc = T.hdr[c];
+        const int ndo = hc.z - hc.x, mc = hc.y - hc.x;
+        const double* uc = T.upd + T.loff[c];
+        const int32_t* rm = P.rmap + P.rmap_ptr[c];
+        for (int xx = threadIdx.x; xx < mc; xx += ST_T) {
+            int pos;
+            if (xx < ndo) pos = p + dof + xx;
+            else { const int r = rm[xx - ndo]; pos = r < p ? r : r + nd; }
+            yo[pos] += uc[xx];
+        }
+        dof += ndo;
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < f; i += ST_T) y[i] = i < q ? yo[T.perm[qo + i]] : yo[i];
     __syncthreads();
     for (int t = 0; t < e; ++t) {
         const double yt = y[t];
@@ -119,14 +148,16 @@ __global__ void __launch_bounds__(ST_T) k_fwd(StorePlan T, const int32_t* __rest
         }
         x[lab[t]] = z;
     }
-    for (int i = e + threadIdx.x; i < f; i += ST_T) atomicAdd(&x[lab[i]], y[i]);
+    double* us = T.upd + T.loff[s];                                      // update vector: rows e..f
+    for (int i = e + threadIdx.x; i < f; i += ST_T) us[i - e] = y[i];
 }
 
 // back substitution for the fronts of one level (levels top-down)
 __global__ void __launch_bounds__(ST_T) k_bwd(StorePlan T, const int32_t* __restrict__ fronts, double* __restrict__ x) {
-    extern __shared__ double xs[];
+    extern __shared__ double xsm[];
     __shared__ double red[ST_T / 32];
     const int s = fronts[blockIdx.x];
+    double* xs = T.yoff[s] >= 0 ? T.ybuf + T.yoff[s] : xsm;
     const int4 h = T.hdr[s];
     const int e = h.x, f = h.y;
     const double* L = T.panel + T.poff[s];
@@ -167,18 +198,21 @@ static void set_smem_attr() {
     cudaFuncSetAttribute(k_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
-int solve_max_front() { return 200 * 1024 / 8; }
+int solve_max_front() { return 200 * 1024 / 16; }     // k_fwd keeps two vectors of f doubles
 
-void launch_fwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st) {
+void launch_fwd(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x,
+                cudaStream_t st) {
     if (nfronts <= 0) return;
     set_smem_attr();
-    k_fwd<<<nfronts, ST_T, (size_t)fmax * sizeof(double), st>>>(T, fronts, x);
+    const int fs = std::min(fmax, solve_max_front());
+    k_fwd<<<nfronts, ST_T, (size_t)2 * fs * sizeof(double), st>>>(P, T, fronts, x);
 }
 
 void launch_bwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st) {
     if (nfronts <= 0) return;
     set_smem_attr();
-    k_bwd<<<nfronts, ST_T, (size_t)fmax * sizeof(double), st>>>(T, fronts, x);
+    const int fs = std::min(fmax, solve_max_front());
+    k_bwd<<<nfronts, ST_T, (size_t)fs * sizeof(double), st>>>(T, fronts, x);
 }
 
 }  // namespace kep

@@ -172,3 +172,29 @@ def test_c1_report_tables():
     assert all(a >= b for (_, _, a), (_, _, b) in zip(tr, tr[1:]))              # m never grows
     assert 0 < t6["bound"] <= t6["residual"] <= rep["stage3_iters"]
     assert t6["bound"] < t6["difference"] <= rep["stage3_iters"]
+
+
+def test_c3_three_stage_validated():
+    """BASELINE c3 (n = 243,000, BASELINE.json configs[2] "full 3-stage solve"): Alg. 4 end to end --
+    stage 1 (Alg. 2), stage 2 (multisection, 16 shifts per round), stage 3 (Alg. 3 SI Lanczos with
+    kep_solve on the retained factor).  lambda_k is validated by nu (index), by its residual and by the
+    bound Eq. (3.1); the Table 4/5/6 analogues are reported."""
+    import scipy.sparse as sp
+    p = kepgen.config(3)
+    k = Kep.from_pencil(p, max_batch=16)
+    k.set_values(p.a, p.b)
+    kk = int(0.25 * p.n)
+    lam, x, rep = k.kth_eigenpair(kk, shifts_per_round=16)
+    print({t: rep[t] for t in ("table4", "table5", "table6", "stage1_iters", "stage2_rounds", "stage3_iters",
+                               "seconds", "rel_residual", "eta")})
+    assert rep["status"] == KEP_OK, rep
+    _validate_index(k, p, lam, kk)
+    n = p.n
+    Lo_a = sp.csc_matrix((p.a, p.rowidx, p.colptr), shape=(n, n))
+    Lo_b = sp.csc_matrix((p.b, p.rowidx, p.colptr), shape=(n, n))
+    Af = Lo_a + sp.tril(Lo_a, -1).T
+    Bf = Lo_b + sp.tril(Lo_b, -1).T
+    assert np.linalg.norm(Af @ x - lam * (Bf @ x)) / np.linalg.norm(x) < 1e-9
+    assert abs(x @ (Bf @ x) - 1.0) < 1e-9
+    assert rep["eta"] <= 1e-10 * abs(lam) + 1e-14
+    assert rep["table5"]["m"] <= 20 and 0 < rep["table6"]["bound"] <= rep["stage3_iters"]
