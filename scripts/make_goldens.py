@@ -25,11 +25,11 @@ _SO = None
 _NB = 0
 
 
-def _init(cfg, nb):
+def _init(cfg, nb, threads):
     global _P, _SO, _NB
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
     from threadpoolctl import threadpool_limits
-    threadpool_limits(1)
+    threadpool_limits(threads)
     import kepgen
     from oracle.sparse_mf import SparseOracle
     _P = kepgen.config(cfg)
@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--shifts", type=int, default=8)
     ap.add_argument("--procs", type=int, default=8)
     ap.add_argument("--reuse", default=None)
+    ap.add_argument("--threads", type=int, default=1, help="BLAS threads per worker process")
     ap.add_argument("--nb", type=int, default=None,
                     help="O-sparse FS panel width (0 = unblocked loop); default 64 for c3 and c5, else 0")
     a = ap.parse_args()
@@ -67,8 +68,8 @@ def main():
         for s in sig:
             todo += [s - d] + ([] if float(s) in old else [s]) + [s + d]
         nb = a.nb if a.nb is not None else (64 if cfg in (3, 5) else 0)
-        with get_context("fork").Pool(a.procs, initializer=_init, initargs=(cfg, nb)) as pool:
-            res = pool.map(_nu, todo)
+        with get_context("fork").Pool(a.procs, initializer=_init, initargs=(cfg, nb, a.threads)) as pool:
+            res = pool.map(_nu, todo, chunksize=1)
         out = []
         it = iter(res)
         for s in sig:
