@@ -79,6 +79,8 @@ struct kep_ctx {
     std::vector<std::vector<FsGroup>> fs_groups;   // per level: fast fronts by FS capacity (k_fsp/k_fsu passes)
     int4* d_aitems = nullptr;                   // k_assemble strips (front, x, S, 0): all fronts, then fast fronts
     std::vector<int64_t> aitem_off, aitem_cnt, raitem_off, raitem_cnt;
+    int4* d_smitems = nullptr;                  // k_asm_smem strips (front, x, S, 0) per level
+    std::vector<int64_t> smitem_off, smitem_cnt;
     std::vector<char> asm_red;                  // per level: small fronts, k_assemble_red
     std::vector<int64_t> fast_off, fast_cnt, ref_off, ref_cnt, item_off, item_cnt, litem_off, litem_cnt;
     // fast-path pivot records: per-front offsets (entries), per shift stride (doubles)
@@ -164,6 +166,7 @@ namespace {
 thread_local std::string g_err;
 constexpr int kReruns = 2;      // fast-path reruns per level before the unblocked fallback
 constexpr int kSmallDelay = 8;  // k_small eligibility: the panel with this many delayed-in columns fits kSmallCap
+constexpr int kAsmSmemCap = 2048;   // k_asm_smem on levels whose fronts all have at most this capacity
 constexpr int kBigQ = 2048;        // big fronts: FS capacity at least this (c4 root, 1216: faster on k_fsp) ...
 constexpr int kBigGroups = 74;      // ... on levels with at most this many (front, shift) groups (>= 2 SMs each)
 constexpr int kSmallMaxPiv = 16;   // k_small: fronts with at most this many own pivots
@@ -325,7 +328,8 @@ kep_status build_lists(kep_ctx* c) {
     c->xfront_off.assign(nl, 0); c->xfront_cnt.assign(nl, 0);
     c->aitem_off.assign(nl, 0); c->aitem_cnt.assign(nl, 0);
     c->raitem_off.assign(nl, 0); c->raitem_cnt.assign(nl, 0);
-    std::vector<int4> aitems;
+    std::vector<int4> aitems, smitems;
+    c->smitem_off.assign(nl, 0); c->smitem_cnt.assign(nl, 0);
     auto strips = [&](int s, int rmax) {              // rmax: CTAs per front (k_reassemble loops)
         const int ns = kep::assembly_strips((int)S.forder[s]);
         const int r = std::min(ns, rmax);
@@ -359,6 +363,20 @@ kep_status build_lists(kep_ctx* c) {
         }
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) strips(S.level_fronts[k], INT_MAX);
         c->aitem_cnt[L] = (int64_t)aitems.size() - c->aitem_off[L];
+        {   // shared-memory strip assembly where every front of the level is small enough
+            bool ok = getenv("KEP_ASM_SMEM") != nullptr;       // opt-in: measured slower than the RED / gather
+                                                               // kernels at c4 (137 vs 107 ms per 8 shifts)
+            for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1] && ok; ++k)
+                ok = S.capacity[S.level_fronts[k]] <= kAsmSmemCap;
+            c->smitem_off[L] = (int64_t)smitems.size();
+            if (ok)
+                for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
+                    const int s = S.level_fronts[k];
+                    const int ns = kep::smem_strips(S.capacity[s]);
+                    for (int x = 0; x < ns; ++x) smitems.push_back(make_int4(s, x, ns, 0));
+                }
+            c->smitem_cnt[L] = (int64_t)smitems.size() - c->smitem_off[L];
+        }
         c->raitem_off[L] = (int64_t)aitems.size();
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k)
             if (is_fast(S.level_fronts[k])) {
@@ -568,6 +586,8 @@ kep_status build_lists(kep_ctx* c) {
     }
     cudaFree(c->d_aitems); c->d_aitems = nullptr;
     KEP_CUDA(c, upload(&c->d_aitems, aitems));
+    cudaFree(c->d_smitems); c->d_smitems = nullptr;
+    KEP_CUDA(c, upload(&c->d_smitems, smitems));
     // pivot-record offsets: Q_s = p_s + slack entries per front
     std::vector<int64_t> aoff(S.nf > 0 ? S.nf : 1, 0);
     int64_t acc = 0;
@@ -851,7 +871,8 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             const int b = S.level_ptr[L], nfl = S.level_ptr[L + 1] - b;
             cur_level = L;
             mark(KEP_K_ASSEMBLE, true);
-            if (c->asm_red[L]) kep::launch_assemble_red(P, c->d_level_fronts + b, nfl, m, c->stream);
+            if (c->smitem_cnt[L]) kep::launch_asm_smem(P, c->d_smitems + c->smitem_off[L], (int)c->smitem_cnt[L], m, c->stream);
+            else if (c->asm_red[L]) kep::launch_assemble_red(P, c->d_level_fronts + b, nfl, m, c->stream);
             else kep::launch_assemble(P, c->d_aitems + c->aitem_off[L], (int)c->aitem_cnt[L], m, false, c->stream);
             mark(KEP_K_ASSEMBLE, false);
             if (resid) kep::launch_capture(P, c->d_level_fronts + b, nfl, c->d_f0, c->stream);
@@ -1946,7 +1967,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1], c->d_rr_l[2], c->d_rr_u, c->d_rr_a, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
                         c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small, c->d_f0, c->d_resid, c->d_ritems,
                         c->d_smfronts, c->d_tmaps, c->d_tmap_idx, c->d_big_groups, c->d_big_scroff, c->d_big_scr,
-                        c->d_big_state, c->d_big_bars};
+                        c->d_big_state, c->d_big_bars, c->d_smitems};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

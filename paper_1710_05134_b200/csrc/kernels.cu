@@ -557,6 +557,168 @@ __device__ __forceinline__ void assemble_front_red(const DevPlan& P, const int32
     }
 }
 
+// ---------------------------------------------------------------- a1 + a2, shared-memory strips
+// One CTA per strip of a front (columns [clo, chi), at most kSmStripEnt lower entries): the strip
+// is built in shared memory -- zero, the original entries (alpha a - sigma b), then each child's
+// entries landing in it, children in order (one writer per entry and child: plain adds, no
+// atomics; deterministic) -- and stored once, column by column, coalesced.  HBM traffic is the
+// ideal one: 8 B written per front entry, every child entry read once (by the CTA owning its
+// parent column), no zero-fill pass, no read-modify-write.
+constexpr int kSmStripEnt = 4096;         // doubles of shared memory per strip (32 KB)
+constexpr int kSmMap = 4096;              // child positions staged in shared memory
+
+__global__ void __launch_bounds__(kAsmRedThreads, 5) k_asm_smem(DevPlan P, const int4* __restrict__ items) {
+    extern __shared__ double sbuf[];                           // [kSmStripEnt]
+    __shared__ uint16_t s_pos[kSmMap];
+    __shared__ int s_nd, s_skip;
+    __shared__ double s_red[32];
+    const int4 itm = items[blockIdx.x];
+    const int s = itm.x, xs = itm.y, S = itm.z;
+    const int sh = blockIdx.y;
+    ShiftStat* st = P.stats + sh;
+    double* arena = P.arena + (size_t)sh * P.arena_stride;
+    int32_t* nd_in = P.nd_in + (size_t)sh * P.nf;
+    const int32_t* nd_out = P.nd_out + (size_t)sh * P.nf;
+    int32_t* doff = P.doff + (size_t)sh * P.nf;
+    const int c0 = P.child_ptr[s], c1 = P.child_ptr[s + 1];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kAsmRedThreads / 32;
+    if (tid == 0) {
+        int off = 0, bad = 0;
+        for (int q = c0; q < c1; ++q) {
+            const int c = P.child_list[q];
+            const int no = nd_out[c];
+            if (no < 0) bad = 1;
+            if (xs == 0) doff[c] = off;
+            off += no > 0 ? no : 0;
+        }
+        const int need = P.forder[s] + off;
+        if (need > P.cap[s]) {
+            bad = 1;
+            if (xs == 0) atomicMax(&st->need_slack, off);
+        }
+        if (bad && xs == 0) atomicOr(&st->flags, FLAG_OVERFLOW);
+        s_skip = bad;
+        s_nd = off;
+        if (xs == 0) nd_in[s] = bad ? -1 : off;
+    }
+    __syncthreads();
+    if (s_skip) return;
+    const int nd = s_nd, p = P.npiv[s], fo = P.forder[s] + nd, ld = ldpad(P.cap[s]);
+    double* F = arena + P.arena_off[s];
+    if (xs == 0) {   // labels of the FS positions: own pivots, then each child's delayed variables
+        const AuxRec A = aux_rec(P, sh, s, P.cap[s] - P.ncb[s]);
+        for (int i = tid; i < p; i += kAsmRedThreads) A.label[i] = P.piv_first[s] + i;
+        int off = 0;
+        for (int q = c0; q < c1; ++q) {
+            const int c = P.child_list[q];
+            const int ndo = nd_out[c];
+            if (ndo <= 0) continue;
+            const AuxRec C = aux_rec(P, sh, c, P.cap[c] - P.ncb[c]);
+            const int ec = P.npiv[c] + nd_in[c] - ndo;
+            for (int j = tid; j < ndo; j += kAsmRedThreads) A.label[p + off + j] = C.label[C.perm[ec + j]];
+            off += ndo;
+        }
+    }
+    int clo, chi;
+    tri_split(fo, S, xs, clo, chi);
+    // entry offset of column j (row j) inside the strip
+    auto colbase = [&](int j) -> int {
+        return (int)((int64_t)(j - clo) * fo - (((int64_t)j * (j - 1) - (int64_t)clo * (clo - 1)) >> 1));
+    };
+    const int ent = colbase(chi);
+    for (int x = tid; x < ent; x += kAsmRedThreads) sbuf[x] = 0.0;
+    __syncthreads();
+    const double sigma = P.sigma[sh], alpha = P.alpha[sh];
+    double mx = 0.0;
+    {   // original entries of the strip's columns (asm_col: first entry of each local pivot column)
+        const int64_t a0 = P.asm_ptr[s];
+        const int32_t* acol = P.asm_col + P.piv_first[s] + s;
+        const int jl = min(clo, p), jh = min(chi, p);
+        const int64_t k0 = a0 + acol[jl], k1 = a0 + acol[jh];
+        for (int64_t k = k0 + tid; k < k1; k += kAsmRedThreads) {
+            const uint32_t rc = P.asm_rc[k];
+            const int lr = (int)(rc >> 16), lc = (int)(rc & 0xffffu);
+            const int r = lr < p ? lr : lr + nd;
+            const double v = fma(-sigma, P.b[k], alpha * P.a[k]);
+            sbuf[colbase(lc) + (r - lc)] = v;
+            mx = fmax(mx, fabs(v));
+        }
+    }
+    mx = block_max<kAsmRedThreads>(mx, s_red);               // (barrier: originals are in)
+    if (tid == 0 && mx > 0.0) atomic_max_pos_double(&st->smax_bits, mx);
+    int off = 0;
+    for (int q = c0; q < c1; ++q) {
+        const int c = P.child_list[q];
+        const int ndo = nd_out[c] > 0 ? nd_out[c] : 0;
+        const int fc = P.forder[c] + nd_in[c];
+        const int ldc = ldpad(P.cap[c]);
+        const int mc = ndo + P.ncb[c];
+        const int ec = fc - mc;
+        const double* __restrict__ Fc = arena + P.arena_off[c];
+        const bool wup = P.flag[(size_t)sh * P.nf + c] == FL_OK && ndo > 0;
+        const int32_t* __restrict__ rm = P.rmap + P.rmap_ptr[c];
+        const int dof = p + off;
+        off += ndo;
+        const bool staged = mc <= kSmMap;
+        __syncthreads();                                      // previous child's adds and s_pos reads done
+        if (staged)
+            for (int x = tid; x < mc; x += kAsmRedThreads) {
+                int v;
+                if (x < ndo) v = dof + x;
+                else { const int r = rm[x - ndo]; v = r < p ? r : r + nd; }
+                s_pos[x] = (uint16_t)v;
+            }
+        __syncthreads();
+        auto pos = [&](int x) -> int {
+            if (staged) return s_pos[x];
+            if (x < ndo) return dof + x;
+            const int r = rm[x - ndo];
+            return r < p ? r : r + nd;
+        };
+        // non-delayed child columns landing in the strip: a contiguous range (positions increase)
+        int xa = ndo, xb = mc;
+        {
+            int lo = ndo, hi = mc;                            // first x with pos(x) >= clo
+            while (lo < hi) { const int m = (lo + hi) >> 1; if (pos(m) < clo) lo = m + 1; else hi = m; }
+            xa = lo;
+            hi = mc;                                          // first x with pos(x) >= chi
+            while (lo < hi) { const int m = (lo + hi) >> 1; if (pos(m) < chi) lo = m + 1; else hi = m; }
+            xb = lo;
+        }
+        for (int x = xa + warp; x < xb; x += nw) {
+            const int pj = pos(x);
+            const int cb = colbase(pj) - pj;
+            const double* __restrict__ colc = Fc + (size_t)(ec + x) * ldc + ec;
+            constexpr int U = 4;                              // loads in flight per lane
+            for (int y0 = x + lane; y0 < mc; y0 += 32 * U) {
+                double v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) { const int y = y0 + 32 * u; v[u] = y < mc ? __ldg(colc + y) : 0.0; }
+#pragma unroll
+                for (int u = 0; u < U; ++u) { const int y = y0 + 32 * u; if (y < mc) sbuf[cb + pos(y)] += v[u]; }
+            }
+        }
+        // delayed columns (rare): every entry filtered by its lower-triangle column
+        for (int x = warp; x < ndo; x += nw) {
+            const int pj = pos(x);
+            for (int y = x + lane; y < mc; y += 32) {
+                const int pi = pos(y);
+                const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
+                if (lo < clo || lo >= chi) continue;
+                const double v = (wup && y >= ndo) ? Fc[(ec + x) + (size_t)(ec + y) * ldc]
+                                                   : Fc[(ec + y) + (size_t)(ec + x) * ldc];
+                sbuf[colbase(lo) + (hi - lo)] += v;
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = clo + warp; j < chi; j += nw) {               // one coalesced store per column
+        const int cb = colbase(j) - j;
+        double* __restrict__ Fj = F + (size_t)j * ld;
+        for (int i = j + lane; i < fo; i += 32) Fj[i] = sbuf[cb + i];
+    }
+}
+
 __global__ void __launch_bounds__(kAsmRedThreads) k_assemble_red(DevPlan P, const int32_t* __restrict__ list, int S) {
     assemble_front_red(P, list, S, 0);
 }
@@ -784,6 +946,20 @@ void launch_assemble(const DevPlan& P, const int4* items, int nitems, int batch,
     }
     if (only_flagged) k_reassemble<<<dim3(nitems, batch), kAsmThreads, smem, st>>>(P, items);
     else k_assemble<<<dim3(nitems, batch), kAsmThreads, smem, st>>>(P, items);
+}
+
+int smem_strips(int cap) {
+    const int64_t T = (int64_t)cap * (cap + 1) / 2;
+    const int64_t room = kSmStripEnt - cap;                    // a strip holds T / S entries + one column
+    return room <= 0 ? 0 : (int)std::max<int64_t>(1, (T + room - 1) / room);
+}
+
+void launch_asm_smem(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st) {
+    if (nitems <= 0) return;
+    const size_t smem = sizeof(double) * kSmStripEnt;
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) cudaFuncSetAttribute(k_asm_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_asm_smem<<<dim3(nitems, batch), kAsmRedThreads, smem, st>>>(P, items);
 }
 
 int assembly_strips(int forder) {

@@ -7,6 +7,7 @@
 // FP64 tensor-core inner product (mma.sync m8n8k4 f64 = SASS DMMA).
 // Storage: L[i,t] at F[i + t*ld] (lower), W[i,t] at F[t + i*ld] (upper).
 #include <cfloat>
+#include <cstdlib>
 #include <climits>
 #include <cstdint>
 
@@ -265,6 +266,7 @@ constexpr int SS_C = 256;       // max CB order
 constexpr int SS_K = 48;        // max eliminated pivots
 constexpr int SS_P = SS_K + 4;  // = 4 (mod 16)
 
+template <bool RED>
 __global__ void __launch_bounds__(SS_T) k_schur_small(DevPlan P, const int32_t* __restrict__ fronts) {
     extern __shared__ __align__(16) double Gs[];        // [SS_C][SS_P]
     __shared__ unsigned long long Sg[SS_K];
@@ -331,7 +333,11 @@ __global__ void __launch_bounds__(SS_T) k_schur_small(DevPlan P, const int32_t* 
                 for (int h = 0; h < 2; ++h) {
                     const int i = i0 + 8 * mb + g;
                     const int j = j0 + 8 * nb + 2 * tg + h;
-                    if (i < c && j < c && i >= j) atomicAdd(&F[(q + i) + (size_t)(q + j) * ld], -acc[mb][nb][h]);
+                    if (i < c && j < c && i >= j) {
+                        double* x = &F[(q + i) + (size_t)(q + j) * ld];
+                        if (RED) atomicAdd(x, -acc[mb][nb][h]);
+                        else *x -= acc[mb][nb][h];                     // the tile's only writer
+                    }
                 }
     }
 }
@@ -382,7 +388,12 @@ void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, in
     if (nfronts <= 0) return;
     const size_t smem = sizeof(double) * SS_C * SS_P;
     static unsigned long long attr = 0;
-    if (first_on_device(attr)) { cudaFuncSetAttribute(k_schur_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  }
-    k_schur_small<<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts);
+    if (first_on_device(attr)) {
+        cudaFuncSetAttribute(k_schur_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_schur_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    static const bool red = getenv("KEP_SCHUR_NORED") == nullptr;   // RED measured 2.6x faster at c4 level 0
+    if (red) k_schur_small<true><<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts);
+    else k_schur_small<false><<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts);
 }
 }  // namespace kep
