@@ -27,29 +27,34 @@ def cached(cfg, shape=None):
     return p, lo, hi
 
 
-cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-m = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
-shape = tuple(int(x) for x in sys.argv[4].split("x")) if len(sys.argv) > 4 else None
-t = time.time()
-p, lo, hi = cached(cfg, shape)
-print(f"gen {time.time() - t:.1f}s n={p.n}", flush=True)
-k = Kep.from_pencil(p, max_batch=m, profile=True)
-a = k.analysis()
-print({x: a[x] for x in ("n_fronts", "n_levels", "max_front", "flops", "arena_bytes", "batch")}, flush=True)
-k.set_values(p.a, p.b)
-sig = kepgen.uniform_shifts(lo, hi, m)
-k.inertia_many(sig)
-k.reset_profile()
-import torch  # noqa: E402
-torch.cuda.synchronize()
-t = time.time()
-for _ in range(reps):
-    nus, st, infos = k.inertia_many(sig, with_info=True)
-dt = time.time() - t
-pr = k.profile()
-print(f"{m * reps / dt:.3f} shifts/s wall ({dt / reps * 1e3:.1f} ms per {m} shifts); redo/shift "
-      f"{np.mean([i.n_redo for i in infos]):.1f} delayed/shift {np.mean([i.n_delayed for i in infos]):.1f}")
-print({kk: round(v / reps, 2) for kk, v in pr["ms"].items()}, "launches", {kk: v // reps for kk, v in pr["launches"].items()})
-print("schur TF/s", pr["schur_flops"] / (pr["ms"]["schur"] / 1e3) / 1e12)
-k.close()
+def main():
+    cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    m = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    shape = tuple(int(x) for x in sys.argv[4].split("x")) if len(sys.argv) > 4 else None
+    t = time.time()
+    p, lo, hi = cached(cfg, shape)
+    print(f"gen {time.time() - t:.1f}s n={p.n}", flush=True)
+    k = Kep.from_pencil(p, max_batch=m, profile=True)
+    a = k.analysis()
+    print({x: a[x] for x in ("n_fronts", "n_levels", "max_front", "flops", "arena_bytes", "batch")}, flush=True)
+    k.set_values(p.a, p.b)
+    sig = kepgen.uniform_shifts(lo, hi, m)
+    k.inertia_many(sig)
+    k.reset_profile()
+    import torch  # noqa: E402
+    torch.cuda.synchronize()
+    t = time.time()
+    for _ in range(reps):
+        nus, st, infos = k.inertia_many(sig, with_info=True)
+    dt = time.time() - t
+    pr = k.profile()
+    print(f"{m * reps / dt:.3f} shifts/s wall ({dt / reps * 1e3:.1f} ms per {m} shifts); redo/shift "
+          f"{np.mean([i.n_redo for i in infos]):.1f} delayed/shift {np.mean([i.n_delayed for i in infos]):.1f}")
+    print({kk: round(v / reps, 2) for kk, v in pr["ms"].items()}, "launches", {kk: v // reps for kk, v in pr["launches"].items()})
+    print("schur TF/s", pr["schur_flops"] / (pr["ms"]["schur"] / 1e3) / 1e12)
+    k.close()
+
+
+if __name__ == "__main__":
+    main()
