@@ -144,23 +144,27 @@ def _oracle_worker(sigma):
 
 
 class OracleSample:
-    """The oracle as it stands on a bounded sample of the workload, C worker processes."""
+    """The oracle as it stands on a bounded sample of the workload (or, length=None, on the full
+    workload itself), C worker processes."""
 
-    def __init__(self, cfg: int, length: int):
+    def __init__(self, cfg: int, length, pencil=None, bounds=None):
         import kepgen
         from oracle.sparse_mf import SparseOracle
         global _SAMPLE
         if cfg != 4:
             raise ValueError("the CPU sample is defined for the c4 workload")
         base = kepgen.CONFIGS[cfg]["shape"]
-        self.shape = (base[0], base[1], length)
-        p = kepgen.config(cfg, shape=self.shape)
+        self.shape = tuple(base) if length is None else (base[0], base[1], length)
+        p = pencil if (pencil is not None and length is None) else kepgen.config(cfg, shape=None if length is None else self.shape)
         self.n = p.n
         _SAMPLE = SparseOracle(p)
-        lo, hi = kepgen.spectral_bounds(p)
+        lo, hi = bounds if (bounds is not None and length is None) else kepgen.spectral_bounds(p)
         self.lo, self.hi = lo, hi
-        fl = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_flops.json")))[f"c{cfg}"]
-        self.scale = fl["full"] / fl["x".join(map(str, self.shape))]     # sample shifts per full-size shift
+        if length is None:
+            self.scale = 1.0
+        else:
+            fl = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_flops.json")))[f"c{cfg}"]
+            self.scale = fl["full"] / fl["x".join(map(str, self.shape))]     # sample shifts per full-size shift
         self.cores = len(os.sched_getaffinity(0))
         from multiprocessing import get_context
         self.pool = get_context("fork").Pool(self.cores, initializer=_oracle_worker_init)
@@ -175,6 +179,9 @@ class OracleSample:
         return time.time() - t, [r[0] for r in res]
 
     def describe(self):
+        if self.scale == 1.0:
+            return (f"c4 at full size (n={self.n}), one shift per core on {self.cores} cores in parallel, 1 BLAS "
+                    f"thread each; measured, not scaled")
         return (f"c4 recipe on a {'x'.join(map(str, self.shape))} periodic sub-wire (n={self.n}), one shift per "
                 f"core on {self.cores} cores in parallel, 1 BLAS thread each; wall time scaled to full-size "
                 f"c4 shifts by the oracle's own flop ratio x{self.scale:.2f} (tests/golden/oracle_flops.json)")
@@ -215,8 +222,8 @@ def run_reference(args, rank, world):
     return 0
 
 
-def cpu_baseline_leg(cfg, length):
-    smp = OracleSample(cfg, length)
+def cpu_baseline_leg(cfg, length, pencil=None, bounds=None):
+    smp = OracleSample(cfg, length, pencil, bounds)
     wall, ts = smp.step(0)
     smp.close()
     v = smp.cores / smp.scale / wall
@@ -251,6 +258,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-length", type=int, default=150, help="sub-wire length of the cpu_baseline sample")
     ap.add_argument("--ref-length", type=int, default=100, help="sub-wire length of the reference-arm sample")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="cpu_baseline on the full-size c4 pencil (C shifts in parallel, ~15 min of host time)")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -271,6 +280,7 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # NCCL init log (transport, NVLS) on stderr
         dist.init_process_group("nccl", device_id=dev)
 
     def log(*a):
@@ -411,7 +421,11 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == 4 and not args.shape:
-        cpu = cpu_baseline_leg(args.config, args.cpu_length)
+        if args.cpu_full:
+            del k                                      # free device memory is irrelevant; host RAM is not
+            cpu = cpu_baseline_leg(args.config, None, p, (meta["lo"], meta["hi"]))
+        else:
+            cpu = cpu_baseline_leg(args.config, args.cpu_length)
 
     if rank == 0:
         msd = prof["ms"]
