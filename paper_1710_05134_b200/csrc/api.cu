@@ -150,6 +150,9 @@ struct kep_factorization {
     double *upd = nullptr, *ybuf = nullptr;                 // solve scratch (update vectors, big fronts' vectors)
     std::vector<int64_t> h_poff, h_loff, h_qoff, h_yoff;
     std::vector<int> level_fmax;                 // per level: max front capacity (shared memory of the solves)
+    std::vector<int64_t> big_off, big_cnt;       // per level: fronts solved by the blocked kernels
+    std::vector<int> big_fmax, big_emax;
+    int32_t* d_bigf = nullptr;
     double *xw = nullptr, *bw = nullptr;         // work vectors (n)
     int64_t panel_doubles = 0, lab_ints = 0, q_entries = 0;
     kep::StorePlan plan() const {
@@ -781,11 +784,11 @@ DevPlan make_plan(kep_ctx* c) {
 
 void free_store(kep_factorization* k) {
     void* ptrs[] = {k->panel, k->lab, k->d, k->ds, k->kind, k->perm, k->hdr, k->poff, k->loff, k->qoff, k->yoff,
-                    k->upd, k->ybuf};
+                    k->upd, k->ybuf, k->d_bigf};
     for (void* q : ptrs) cudaFree(q);
     k->panel = nullptr; k->lab = nullptr; k->d = nullptr; k->ds = nullptr; k->kind = nullptr; k->perm = nullptr;
     k->hdr = nullptr; k->poff = nullptr; k->loff = nullptr; k->qoff = nullptr; k->yoff = nullptr;
-    k->upd = nullptr; k->ybuf = nullptr;
+    k->upd = nullptr; k->ybuf = nullptr; k->d_bigf = nullptr;
 }
 
 // (Re)allocate the factor store for the current memory plan (capacities).
@@ -808,13 +811,28 @@ kep_status prepare_store(kep_ctx* c, kep_factorization* k) {
     KEP_CUDA(c, cudaMalloc(&k->perm, std::max<int64_t>(qo, 1) * sizeof(int32_t)));
     KEP_CUDA(c, cudaMalloc(&k->upd, std::max<int64_t>(lo, 1) * sizeof(double)));
     KEP_CUDA(c, cudaMalloc(&k->hdr, std::max<int64_t>(S.nf, 1) * sizeof(int4)));
-    {   // fronts beyond the shared-memory solve vectors: global front vectors (2 f doubles each)
+    {   // large fronts: blocked multi-CTA solves with global front vectors (2 f doubles each)
         k->h_yoff.assign(std::max<int64_t>(S.nf, 1), -1);
         int64_t yo = 0;
         for (int64_t s = 0; s < S.nf; ++s)
-            if (S.capacity[s] > kep::solve_max_front()) { k->h_yoff[s] = yo; yo += 2 * (int64_t)S.capacity[s]; }
+            if (S.capacity[s] > kep::solve_big_front()) { k->h_yoff[s] = yo; yo += 2 * (int64_t)S.capacity[s]; }
         KEP_CUDA(c, cudaMalloc(&k->ybuf, std::max<int64_t>(yo, 1) * sizeof(double)));
         KEP_CUDA(c, upload(&k->yoff, k->h_yoff));
+        const int nlv = (int)S.level_ptr.size() - 1;
+        std::vector<int32_t> bl;
+        k->big_off.assign(nlv, 0); k->big_cnt.assign(nlv, 0); k->big_fmax.assign(nlv, 0); k->big_emax.assign(nlv, 0);
+        for (int L = 0; L < nlv; ++L) {
+            k->big_off[L] = (int64_t)bl.size();
+            for (int x = S.level_ptr[L]; x < S.level_ptr[L + 1]; ++x) {
+                const int s = S.level_fronts[x];
+                if (k->h_yoff[s] < 0) continue;
+                bl.push_back(s);
+                k->big_fmax[L] = std::max(k->big_fmax[L], (int)S.capacity[s]);
+                k->big_emax[L] = std::max(k->big_emax[L], (int)(S.capacity[s] - S.ncb[s]));
+            }
+            k->big_cnt[L] = (int64_t)bl.size() - k->big_off[L];
+        }
+        KEP_CUDA(c, upload(&k->d_bigf, bl));
     }
     KEP_CUDA(c, upload(&k->poff, k->h_poff));
     KEP_CUDA(c, upload(&k->loff, k->h_loff));
@@ -823,7 +841,8 @@ kep_status prepare_store(kep_ctx* c, kep_factorization* k) {
     k->level_fmax.assign(nl, 0);
     for (int L = 0; L < nl; ++L)
         for (int x = S.level_ptr[L]; x < S.level_ptr[L + 1]; ++x)
-            k->level_fmax[L] = std::max(k->level_fmax[L], (int)S.capacity[S.level_fronts[x]]);
+            if (S.capacity[S.level_fronts[x]] <= kep::solve_big_front())       // large ones: blocked kernels
+                k->level_fmax[L] = std::max(k->level_fmax[L], (int)S.capacity[S.level_fronts[x]]);
     return KEP_OK;
 }
 
@@ -911,6 +930,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 for (int k = 0; k < 3; ++k) R.l[k] = c->d_rr_l[k];
                 R.u = c->d_rr_u; R.a = c->d_rr_a;
                 int32_t rc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                bool anyflag = false;                   // some pass flagged a front (rerun or unblocked kernel)
                 int32_t pend[2] = {0, 0};
                 KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
                 for (int pass = 0; pass <= kReruns; ++pass) {
@@ -983,13 +1003,14 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                     KEP_CUDA(c, cudaStreamSynchronize(c->stream));
                     c->prof.launches[KEP_K_CHECK] += 2;
                     if (rc[5] == 0) break;              // nothing flagged
+                    anyflag = true;
                     mark(KEP_K_CHECK, true);
                     kep::launch_assemble(P, c->d_rr_a, rc[5], m, true, c->stream);
                     mark(KEP_K_CHECK, false);
                     c->prof.launches[KEP_K_CHECK]++;
                     if (rc[0] == 0) break;              // only fronts for the unblocked kernel
                 }
-                if (rc[5] > 0) {                        // fronts left for the unblocked kernel
+                if (anyflag) {                          // fronts left for the unblocked kernel (flag != FL_OK)
                     mark(KEP_K_REF, true);
                     kep::launch_factor_list(P, fl, nfl2, m, c->stream, true);
                     mark(KEP_K_REF, false);
@@ -1383,12 +1404,18 @@ kep_status kep_solve_dev(const kep_factorization* k, const double* b_dev, double
     kep::launch_gather(b_dev, c->d_perm, k->xw, S.n, c->stream);          // to elimination positions
     const kep::StorePlan T = k->plan();
     const DevPlan P = make_plan(c);
-    for (int L = 0; L < nl; ++L)
+    for (int L = 0; L < nl; ++L) {
         kep::launch_fwd(P, T, c->d_level_fronts + S.level_ptr[L], S.level_ptr[L + 1] - S.level_ptr[L], k->level_fmax[L],
                         k->xw, c->stream);
-    for (int L = nl - 1; L >= 0; --L)
+        kep::launch_fwd_big(P, T, k->d_bigf + k->big_off[L], (int)k->big_cnt[L], k->big_fmax[L], k->big_emax[L], k->xw,
+                            c->stream);
+    }
+    for (int L = nl - 1; L >= 0; --L) {
+        kep::launch_bwd_big(T, k->d_bigf + k->big_off[L], (int)k->big_cnt[L], k->big_fmax[L], k->big_emax[L], k->xw,
+                            c->stream);
         kep::launch_bwd(T, c->d_level_fronts + S.level_ptr[L], S.level_ptr[L + 1] - S.level_ptr[L], k->level_fmax[L],
                         k->xw, c->stream);
+    }
     kep::launch_gather(k->xw, c->d_iperm, x_dev, S.n, c->stream);         // back to dofs
     KEP_CUDA(c, cudaGetLastError());
     return KEP_OK;

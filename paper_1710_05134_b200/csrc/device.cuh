@@ -76,7 +76,9 @@ constexpr int AUX_W = 11;        // doubles per position: diag backup, d, ds, fa
                                  // sgn, gca, gcb
 // front states: FL_OK = factorised, FL_REF = hand to the unblocked kernel,
 // FL_RERUN = rerun the fast path with one more forced delay, FL_ACTIVE = in the current fast pass
-constexpr int FL_OK = 0, FL_REF = 1, FL_RERUN = 2, FL_ACTIVE = 3;
+// FL_REFN = handed to the unblocked kernel by this pass's k_check (k_rerun_lists re-assembles it once
+// and turns it into FL_REF)
+constexpr int FL_OK = 0, FL_REF = 1, FL_RERUN = 2, FL_ACTIVE = 3, FL_REFN = 5;
 constexpr int FSTATE_W = 8;
 constexpr int FMAX = 6;          // forced delays per front before falling back to the unblocked kernel
 
@@ -177,7 +179,12 @@ void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, i
 void launch_fwd(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x,
                 cudaStream_t st);
 void launch_bwd(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x, cudaStream_t st);
-int solve_max_front();       // largest front whose solve vector lives in shared memory (larger: global scratch)
+int solve_max_front();       // largest front whose solve vectors fit shared memory
+int solve_big_front();       // fronts larger than this: blocked multi-CTA solves (vectors in global scratch)
+void launch_fwd_big(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, int emax,
+                    double* x, cudaStream_t st);
+void launch_bwd_big(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, int emax, double* x,
+                    cudaStream_t st);
 // kth.cu: Lanczos building blocks
 void launch_spmv2(const int64_t* rp, const int32_t* ci, const double* va, const double* vb, const double* x, double* ya,
                   double* yb, int64_t n, cudaStream_t st);

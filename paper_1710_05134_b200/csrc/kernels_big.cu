@@ -171,9 +171,12 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
     long long c_neg = 0, c_zero = 0, c_pos = 0, c_2x2 = 0;
     auto sync_all = [&]() { ++nbar; gbar(G.bar, nbar * (unsigned)ncta); };
     // symmetric interchange of positions a < b (both < q) in the lower-stored front; each CTA moves a
-    // disjoint share: rows a, b of columns t < a (by t), columns a, b below b and the (a, b) band (by row)
-    auto swap_sym = [&](int a, int b) {
+    // disjoint share: rows a, b of columns t < a (by t; column `skip` left out: it is rewritten right
+    // after), columns a, b below b and the (a, b) band (by own row, the same thread-to-row map as the
+    // G-column stores that follow, so a row's old values are moved before its G entry is written)
+    auto swap_sym = [&](int a, int b, int skip) {
         for (int t = cj * BT + tid; t < a; t += ncta * BT) {
+            if (t == skip) continue;
             double* x = F + a + (size_t)t * ld;
             double* y = F + b + (size_t)t * ld;
             const double v = *x; *x = *y; *y = v;
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
             }
         }
         if (!ok) {                                                   // delay column k (R1)
-            if (qe - 1 != k) swap_sym(k, qe - 1);
+            if (qe - 1 != k) swap_sym(k, qe - 1, -1);
             qe--;
             step++;
             sync_all();
@@ -299,8 +302,7 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
         }
         if (kind == 1) {
             const bool fromr = j != k;
-            if (fromr) swap_sym(k, r);
-            sync_all();
+            if (fromr) swap_sym(k, r, -1);                           // no barrier: see swap_sym
             // pivot column after the interchange: column r's values with rows k and r exchanged
             const double* w = fromr ? G.colr : G.colk;
             const double d = fromr ? G.colr[r] : akks;
@@ -320,8 +322,7 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
             step++;
             sync_all();
         } else {
-            if (r != k + 1) swap_sym(k + 1, r);
-            sync_all();
+            if (r != k + 1) swap_sym(k + 1, r, k);                   // column k is rewritten below
             // columns k, k+1 after the interchange (k+1 <-> r): rows k+1 and r exchanged in both
             auto nk = [&](int i) { return G.colk[i == k + 1 ? r : (i == r ? k + 1 : i)]; };
             auto nr = [&](int i) { return G.colr[i == k + 1 ? r : (i == r ? k + 1 : i)]; };

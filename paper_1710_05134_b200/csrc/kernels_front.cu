@@ -31,7 +31,8 @@
 //          unblocked rule's; inertia is counted and L21 = W21 D^-1 written.
 //          A failure -> the front is assembled again (its children's CBs are
 //          still live during the level) and rerun with a forced delay at the
-//          failing step, or after FMAX reruns handed to k_factor_ref.
+//          failing step; after FMAX forced delays, or once the level's kReruns = 2 rerun passes
+//          (api.cu) are used up, it is handed to k_factor_ref.
 //
 // Storage per front (column-major, ld = f):  L[i,t] at F[i + t*ld] (i > t;
 // 0 at the subdiagonal of a 2x2 block, whose D lives in the aux record),
@@ -965,9 +966,11 @@ __global__ void __launch_bounds__(1024) k_rerun_lists(DevPlan P, const int32_t* 
         const int s = fl[x];
         bool fg = false, fa = false;                    // flagged for a rerun / for a rerun or the unblocked kernel
         for (int sh = 0; sh < batch; ++sh) {
-            const int32_t v = P.flag[(size_t)sh * P.nf + s];
+            int32_t* fp = P.flag + (size_t)sh * P.nf + s;
+            const int32_t v = *fp;
             fg |= v == FL_RERUN;
-            fa |= v == FL_RERUN || v == FL_REF;
+            fa |= v == FL_RERUN || v == FL_REFN;         // newly flagged by this pass only
+            if (v == FL_REFN) *fp = FL_REF;
         }
         if (!fa) continue;
         const int4 a = R.d1[s], b = R.d2[s];           // (l21 mode, l21 off, l21 cnt, uitem off), (ucnt, aoff, acnt, -)
@@ -1105,7 +1108,7 @@ __global__ void __launch_bounds__(FT) k_check(DevPlan P, const int32_t* __restri
                 atomicAdd(P.pending, 1);
                 atomicMax(P.pending + 1, q);                 // largest FS block to rerun (iteration count)
             } else {
-                *flag = FL_REF;
+                *flag = FL_REFN;
             }
             atomicAdd(&st->n_redo, 1ull);
         }

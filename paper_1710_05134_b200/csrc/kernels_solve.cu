@@ -101,13 +101,14 @@ __global__ void __launch_bounds__(ST_T) k_fwd(DevPlan P, StorePlan T, const int3
                                               double* __restrict__ x) {
     extern __shared__ double ysm[];
     const int s = fronts[blockIdx.x];
+    if (T.yoff[s] >= 0) return;                                          // large front: the blocked kernels
     const int4 h = T.hdr[s];
     const int e = h.x, f = h.y, q = h.z;
     const int p = P.npiv[s], nd = q - p;
     const double* L = T.panel + T.poff[s];
     const int* lab = T.lab + T.loff[s];
     const int64_t qo = T.qoff[s];
-    double* yo = T.yoff[s] >= 0 ? T.ybuf + T.yoff[s] : ysm;            // front vector, original local order
+    double* yo = ysm;                                                    // front vector, original local order
     double* y = yo + f;                                                  // pivoted order
     for (int i = threadIdx.x; i < f; i += ST_T) yo[i] = i < p ? x[P.piv_first[s] + i] : 0.0;
     __syncthreads();
@@ -157,7 +158,8 @@ __global__ void __launch_bounds__(ST_T) k_bwd(StorePlan T, const int32_t* __rest
     extern __shared__ double xsm[];
     __shared__ double red[ST_T / 32];
     const int s = fronts[blockIdx.x];
-    double* xs = T.yoff[s] >= 0 ? T.ybuf + T.yoff[s] : xsm;
+    if (T.yoff[s] >= 0) return;                                          // large front: the blocked kernels
+    double* xs = xsm;
     const int4 h = T.hdr[s];
     const int e = h.x, f = h.y;
     const double* L = T.panel + T.poff[s];
@@ -184,6 +186,185 @@ __global__ void __launch_bounds__(ST_T) k_bwd(StorePlan T, const int32_t* __rest
     for (int t = threadIdx.x; t < e; t += ST_T) x[lab[t]] = xs[t];
 }
 
+// ---------------------------------------------------------------- large fronts: blocked solves
+// A front of order f > solve_big_front() solves with all SMs: its vectors live in global scratch
+// (ybuf at yoff: original order [0, f), pivoted order [f, 2f)); the unit lower L11 is processed in
+// 64-column blocks -- the 64 x 64 diagonal block by one CTA, the rows below by a grid of CTAs
+// (forward), or the block's columns against the rows below by one CTA per column (backward, fixed
+// reduction order: deterministic).
+constexpr int SBK = 64;
+
+// forward: extend-add of the children's update vectors into the front vector, then pivot order
+__global__ void __launch_bounds__(ST_T) k_fwdb_prep(DevPlan P, StorePlan T, const int32_t* __restrict__ fronts,
+                                                    const double* __restrict__ x) {
+    const int s = fronts[blockIdx.x];
+    const int4 h = T.hdr[s];
+    const int f = h.y, q = h.z;
+    const int p = P.npiv[s], nd = q - p;
+    const int64_t qo = T.qoff[s];
+    double* yo = T.ybuf + T.yoff[s];
+    double* y = yo + f;
+    for (int i = threadIdx.x; i < f; i += ST_T) yo[i] = i < p ? x[P.piv_first[s] + i] : 0.0;
+    __syncthreads();
+    int dof = 0;
+    for (int k = P.child_ptr[s]; k < P.child_ptr[s + 1]; ++k) {
+        const int c = P.child_list[k];
+        const int4 hc = T.hdr[c];
+        const int ndo = hc.z - hc.x, mc = hc.y - hc.x;
+        const double* uc = T.upd + T.loff[c];
+        const int32_t* rm = P.rmap + P.rmap_ptr[c];
+        for (int xx = threadIdx.x; xx < mc; xx += ST_T) {
+            int pos;
+            if (xx < ndo) pos = p + dof + xx;
+            else { const int r = rm[xx - ndo]; pos = r < p ? r : r + nd; }
+            yo[pos] += uc[xx];
+        }
+        dof += ndo;
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < f; i += ST_T) y[i] = i < q ? yo[T.perm[qo + i]] : yo[i];
+}
+
+// forward, block b: y_b = L_bb^-1 y_b (one warp, the block's L in shared memory)
+__global__ void __launch_bounds__(32) k_fwdb_diag(StorePlan T, const int32_t* __restrict__ fronts, int b) {
+    __shared__ double Lb[SBK][SBK + 1];
+    const int s = fronts[blockIdx.x];
+    const int4 h = T.hdr[s];
+    const int e = h.x, f = h.y;
+    const int t0 = b * SBK;
+    if (t0 >= e) return;
+    const int nb = min(SBK, e - t0);
+    const double* L = T.panel + T.poff[s];
+    double* y = T.ybuf + T.yoff[s] + f;
+    for (int t = 0; t < nb; ++t)
+        for (int i = threadIdx.x; i < nb; i += 32) Lb[i][t] = L[(size_t)(t0 + t) * f + t0 + i];
+    __syncwarp();
+    double v0 = threadIdx.x < nb ? y[t0 + threadIdx.x] : 0.0;
+    double v1 = threadIdx.x + 32 < nb ? y[t0 + 32 + threadIdx.x] : 0.0;
+    for (int t = 0; t < nb; ++t) {
+        const double yt = __shfl_sync(0xffffffffu, t < 32 ? v0 : v1, t & 31);
+        const int i0 = threadIdx.x, i1 = threadIdx.x + 32;
+        if (i0 > t && i0 < nb) v0 = fma(-Lb[i0][t], yt, v0);
+        if (i1 > t && i1 < nb) v1 = fma(-Lb[i1][t], yt, v1);
+    }
+    if (threadIdx.x < nb) y[t0 + threadIdx.x] = v0;
+    if (threadIdx.x + 32 < nb) y[t0 + 32 + threadIdx.x] = v1;
+}
+
+// forward, block b: rows below the block, y[i] -= L[i, block] y_block (grid: front x row chunks)
+__global__ void __launch_bounds__(ST_T) k_fwdb_panel(StorePlan T, const int32_t* __restrict__ fronts, int b) {
+    __shared__ double yb[SBK];
+    const int s = fronts[blockIdx.y];
+    const int4 h = T.hdr[s];
+    const int e = h.x, f = h.y;
+    const int t0 = b * SBK;
+    if (t0 >= e) return;
+    const int nb = min(SBK, e - t0);
+    const int i = t0 + nb + blockIdx.x * ST_T + threadIdx.x;
+    if (t0 + nb + blockIdx.x * ST_T >= f) return;
+    const double* L = T.panel + T.poff[s];
+    double* y = T.ybuf + T.yoff[s] + f;
+    if (threadIdx.x < nb) yb[threadIdx.x] = y[t0 + threadIdx.x];
+    __syncthreads();
+    if (i >= f) return;
+    double acc = 0.0;
+    for (int t = 0; t < nb; ++t) acc = fma(L[(size_t)(t0 + t) * f + i], yb[t], acc);
+    y[i] -= acc;
+}
+
+// forward: D^-1, the eliminated variables' values, the update vector
+__global__ void __launch_bounds__(ST_T) k_fwdb_fin(StorePlan T, const int32_t* __restrict__ fronts, double* __restrict__ x) {
+    const int s = fronts[blockIdx.x];
+    const int4 h = T.hdr[s];
+    const int e = h.x, f = h.y;
+    const int* lab = T.lab + T.loff[s];
+    const int64_t qo = T.qoff[s];
+    const double* y = T.ybuf + T.yoff[s] + f;
+    for (int t = threadIdx.x; t < e; t += ST_T) {
+        const int kd = T.kind[qo + t];
+        double z = 0.0;
+        if (kd == PK_1X1) z = y[t] / T.d[qo + t];
+        else if (kd == PK_2X2A || kd == PK_2X2B) {
+            const int a = kd == PK_2X2A ? t : t - 1;
+            const double d11 = T.d[qo + a], d21 = T.ds[qo + a], d22 = T.d[qo + a + 1];
+            const double det = d11 * d22 - d21 * d21;
+            z = kd == PK_2X2A ? (d22 * y[a] - d21 * y[a + 1]) / det : (d11 * y[a + 1] - d21 * y[a]) / det;
+        }
+        x[lab[t]] = z;
+    }
+    double* us = T.upd + T.loff[s];
+    for (int i = e + threadIdx.x; i < f; i += ST_T) us[i - e] = y[i];
+}
+
+// backward: gather x over the front's rows
+__global__ void __launch_bounds__(ST_T) k_bwdb_prep(StorePlan T, const int32_t* __restrict__ fronts,
+                                                    const double* __restrict__ x) {
+    const int s = fronts[blockIdx.x];
+    const int f = T.hdr[s].y;
+    const int* lab = T.lab + T.loff[s];
+    double* xs = T.ybuf + T.yoff[s];
+    for (int i = threadIdx.x; i < f; i += ST_T) xs[i] = x[lab[i]];
+}
+
+// backward: x[t] -= sum_{i in [r0, r1)} L[i, t] x[i] for the columns t of [c0, c1) (one CTA per column,
+// grid: front x column): rows [r0, r1) = [e, f) (the L21 part) or the L11 rows below a block
+__global__ void __launch_bounds__(ST_T) k_bwdb_cols(StorePlan T, const int32_t* __restrict__ fronts, int b, int l21) {
+    __shared__ double red[ST_T / 32];
+    const int s = fronts[blockIdx.y];
+    const int4 h = T.hdr[s];
+    const int e = h.x, f = h.y;
+    int t, r0, r1;
+    if (l21) { t = blockIdx.x; r0 = e; r1 = f; if (t >= e) return; }
+    else {
+        const int t0 = b * SBK;
+        if (t0 >= e) return;
+        const int nb = min(SBK, e - t0);
+        if ((int)blockIdx.x >= nb) return;
+        t = t0 + blockIdx.x; r0 = t0 + nb; r1 = e;
+    }
+    if (r0 >= r1) return;
+    const double* col = T.panel + T.poff[s] + (size_t)t * f;
+    double* xs = T.ybuf + T.yoff[s];
+    double a = 0.0;
+    for (int i = r0 + threadIdx.x; i < r1; i += ST_T) a = fma(col[i], xs[i], a);
+    a = block_sum(a, red);
+    if (threadIdx.x == 0) xs[t] -= a;
+}
+
+// backward, block b: x_b = L_bb^-T x_b (one warp)
+__global__ void __launch_bounds__(32) k_bwdb_diag(StorePlan T, const int32_t* __restrict__ fronts, int b) {
+    __shared__ double Lb[SBK][SBK + 1];
+    const int s = fronts[blockIdx.x];
+    const int4 h = T.hdr[s];
+    const int e = h.x, f = h.y;
+    const int t0 = b * SBK;
+    if (t0 >= e) return;
+    const int nb = min(SBK, e - t0);
+    const double* L = T.panel + T.poff[s];
+    double* xs = T.ybuf + T.yoff[s];
+    for (int t = 0; t < nb; ++t)
+        for (int i = threadIdx.x; i < nb; i += 32) Lb[i][t] = L[(size_t)(t0 + t) * f + t0 + i];
+    __syncwarp();
+    double v0 = threadIdx.x < nb ? xs[t0 + threadIdx.x] : 0.0;
+    double v1 = threadIdx.x + 32 < nb ? xs[t0 + 32 + threadIdx.x] : 0.0;
+    for (int t = nb - 1; t >= 0; --t) {                      // x_t is final; remove it from rows < t
+        const double xt = __shfl_sync(0xffffffffu, t < 32 ? v0 : v1, t & 31);
+        const int i0 = threadIdx.x, i1 = threadIdx.x + 32;
+        if (i0 < t) v0 = fma(-Lb[t][i0], xt, v0);
+        if (i1 < t) v1 = fma(-Lb[t][i1], xt, v1);
+    }
+    if (threadIdx.x < nb) xs[t0 + threadIdx.x] = v0;
+    if (threadIdx.x + 32 < nb) xs[t0 + 32 + threadIdx.x] = v1;
+}
+
+__global__ void __launch_bounds__(ST_T) k_bwdb_fin(StorePlan T, const int32_t* __restrict__ fronts, double* __restrict__ x) {
+    const int s = fronts[blockIdx.x];
+    const int e = T.hdr[s].x;
+    const int* lab = T.lab + T.loff[s];
+    const double* xs = T.ybuf + T.yoff[s];
+    for (int t = threadIdx.x; t < e; t += ST_T) x[lab[t]] = xs[t];
+}
+
 }  // namespace
 
 void launch_store(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, cudaStream_t st) {
@@ -199,6 +380,34 @@ static void set_smem_attr() {
 }
 
 int solve_max_front() { return 200 * 1024 / 16; }     // k_fwd keeps two vectors of f doubles
+int solve_big_front() { return 2048; }                 // larger fronts: the blocked multi-CTA solves
+
+void launch_fwd_big(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, int emax,
+                    double* x, cudaStream_t st) {
+    if (nfronts <= 0) return;
+    k_fwdb_prep<<<nfronts, ST_T, 0, st>>>(P, T, fronts, x);
+    const int nblk = (emax + SBK - 1) / SBK;
+    for (int b = 0; b < nblk; ++b) {
+        k_fwdb_diag<<<nfronts, 32, 0, st>>>(T, fronts, b);
+        const int rows = fmax - b * SBK;
+        if (rows > 0) k_fwdb_panel<<<dim3((rows + ST_T - 1) / ST_T, nfronts), ST_T, 0, st>>>(T, fronts, b);
+    }
+    k_fwdb_fin<<<nfronts, ST_T, 0, st>>>(T, fronts, x);
+}
+
+void launch_bwd_big(const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, int emax, double* x,
+                    cudaStream_t st) {
+    if (nfronts <= 0) return;
+    (void)fmax;
+    k_bwdb_prep<<<nfronts, ST_T, 0, st>>>(T, fronts, x);
+    k_bwdb_cols<<<dim3(emax, nfronts), ST_T, 0, st>>>(T, fronts, 0, 1);
+    const int nblk = (emax + SBK - 1) / SBK;
+    for (int b = nblk - 1; b >= 0; --b) {
+        k_bwdb_cols<<<dim3(SBK, nfronts), ST_T, 0, st>>>(T, fronts, b, 0);
+        k_bwdb_diag<<<nfronts, 32, 0, st>>>(T, fronts, b);
+    }
+    k_bwdb_fin<<<nfronts, ST_T, 0, st>>>(T, fronts, x);
+}
 
 void launch_fwd(const DevPlan& P, const StorePlan& T, const int32_t* fronts, int nfronts, int fmax, double* x,
                 cudaStream_t st) {
