@@ -38,7 +38,7 @@ namespace {
 
 constexpr double kAlphaB = 0.6403882032022076;   // (1 + sqrt(17)) / 8
 constexpr int BT = 256;                           // k_bigp threads
-constexpr int BNB = 64;                           // pivots per block (the trailing update's K)
+constexpr int BNB = 128;                          // pivots per block (the trailing update's K)
 constexpr int BST_W = 16;                         // state record (int) per group
 
 // state record of a group (global, persists between launches)
@@ -208,6 +208,19 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
             for (int t = 0; t < nt; ++t) v = fma(-gi[(size_t)t * ld], sG[t], v);
             out[i] = v;
         }
+        __syncthreads();                            // the column's own rows are read by other threads next
+    };
+    // group-wide reduction of the CTAs' partials: thread x < ncta loads CTA x's record from L2
+    // (written by other SMs before the barrier), then one CTA reduction
+    auto group_reduce = [&](int base, double& a, int& ai, double& b, double& c) {
+        double va = -1.0, vb = 0.0, vc = 0.0, vd = 0.0;
+        int vi = INT_MAX;
+        if (tid < ncta) {
+            const Part* pp = G.part + base + tid;
+            va = __ldcg(&pp->v0); vb = __ldcg(&pp->v1); vc = __ldcg(&pp->v2); vi = __ldcg(&pp->i0);
+        }
+        cta_reduce(va, vi, vb, vc, vd, sv, si);
+        a = va; ai = vi; b = vb; c = vc;
     };
     while (e < qe && e - k0 < BNB) {
         const int k = e;
@@ -225,14 +238,10 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
         // every CTA has passed a later barrier, i.e. after all reads of it)
         if (tid == 0) G.part[cj] = Part{mC, mR, 0.0, 0.0, iC, 0, 0, 0};
         sync_all();
-        double gC = -1.0, gR = 0.0, akks = 0.0;
+        double gC = -1.0, gR = 0.0, akks = 0.0, zz = 0.0;
         int r = INT_MAX;
-        for (int x = 0; x < ncta; ++x) {
-            const Part pp = G.part[x];
-            part_better(gC, r, pp.v0, pp.i0);
-            gR = fmax(gR, pp.v1);
-        }
-        akks = G.colk[k];                                           // visible after the barrier
+        group_reduce(0, gC, r, gR, zz);
+        akks = __ldcg(G.colk + k);                                  // another CTA's row: visible after the barrier
         const double aakk = fabs(akks);
         if (gC < 0.0) { gC = 0.0; r = k; }
         if (aakk == 0.0 && gR == 0.0) {                             // zero column: exact zero pivot
@@ -265,13 +274,10 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
             if (tid == 0) G.part[ncta + cj] = Part{rho, ra_, gk_, 0.0, 0, 0, 0, 0};
             sync_all();
             double rh = 0.0;
-            for (int x = 0; x < ncta; ++x) {
-                const Part pp = G.part[ncta + x];
-                rh = fmax(rh, pp.v0);
-                rall = fmax(rall, pp.v1);
-                gk = fmax(gk, pp.v2);
-            }
-            arr = fabs(G.colr[r]);
+            int ri = 0;
+            group_reduce(ncta, rh, ri, rall, gk);
+            if (rh < 0.0) rh = 0.0;
+            arr = fabs(__ldcg(G.colr + r));
             if (aakk * rh >= kAlphaB * gC * gC) { kind = 1; j = k; }
             else if (arr >= kAlphaB * rh) { kind = 1; j = r; }
             else { kind = 2; j = r; }
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
                 const double fa = (j == k) ? gR : fmax(rall, gC);
                 ok = (j == k ? aakk : arr) >= u * fa;
             } else {
-                const double a11 = akks, a21 = G.colk[r], a22 = G.colr[r];
+                const double a11 = akks, a21 = __ldcg(G.colk + r), a22 = __ldcg(G.colr + r);
                 const double det = a11 * a22 - a21 * a21;
                 if (det == 0.0) ok = false;
                 else {
@@ -305,10 +311,11 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
             if (fromr) swap_sym(k, r, -1);                           // no barrier: see swap_sym
             // pivot column after the interchange: column r's values with rows k and r exchanged
             const double* w = fromr ? G.colr : G.colk;
-            const double d = fromr ? G.colr[r] : akks;
+            const double d = fromr ? __ldcg(G.colr + r) : akks;
+            const double wk = fromr ? __ldcg(G.colr + k) : 0.0;       // row r of the pivot column
             const double gsc = sqrt(fabs(d)) / d;                    // G = L sqrt|d| = W sqrt|d| / d
             for (int i = max(ra, k + 1) + tid; i < rb; i += BT) {
-                const double wi = (fromr && i == r) ? w[k] : w[i];
+                const double wi = (fromr && i == r) ? wk : w[i];
                 F[i + (size_t)k * ld] = wi * gsc;
             }
             if (cj == 0 && tid == 0) {
@@ -324,8 +331,8 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
         } else {
             if (r != k + 1) swap_sym(k + 1, r, k);                   // column k is rewritten below
             // columns k, k+1 after the interchange (k+1 <-> r): rows k+1 and r exchanged in both
-            auto nk = [&](int i) { return G.colk[i == k + 1 ? r : (i == r ? k + 1 : i)]; };
-            auto nr = [&](int i) { return G.colr[i == k + 1 ? r : (i == r ? k + 1 : i)]; };
+            auto nk = [&](int i) { return __ldcg(G.colk + (i == k + 1 ? r : (i == r ? k + 1 : i))); };
+            auto nr = [&](int i) { return __ldcg(G.colr + (i == k + 1 ? r : (i == r ? k + 1 : i))); };
             const double d11 = nk(k), d21 = nk(k + 1), d22 = nr(k + 1);
             const double det = d11 * d22 - d21 * d21;
             const double i11 = d22 / det, i21 = -d21 / det, i22 = d11 / det;
@@ -369,18 +376,29 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
 
 // ------------------------------------------------------------------ k_bigu
 // F[i, j] -= sum_{t in [k0, e)} G[i, t] S_t G[j, t] for j in [e, q), i in [j, f): 64 x 64 tiles,
-// persistent CTAs over every group's tiles of the level.
+// persistent CTAs over every group's tiles of the level; K streamed in chunks of 16 pivots through a
+// 3-stage cp.async pipeline (G columns are contiguous along the rows: t-major tiles).
 constexpr int UT2 = 128;
-constexpr int UKB = BNB + 1;                     // a 2x2 pair may overfill the block by one
-constexpr int UKP = ((UKB + 3) / 4) * 4;
-constexpr int UPA2 = 64 + 4;
+constexpr int UKC = 16;
+constexpr int UST = 3;
+constexpr int UPA2 = 64 + 4;                     // = 4 (mod 16): conflict-free f64 fragments
 
-__global__ void __launch_bounds__(UT2) k_bigu(DevPlan P, const int2* __restrict__ groups, int ngroups,
-                                              const int64_t* __restrict__ scroff, double* scr, int* state,
-                                              unsigned* bars) {
-    extern __shared__ __align__(16) double ub[];
-    double (*As)[UPA2] = reinterpret_cast<double (*)[UPA2]>(ub);                 // [UKP][68] G[i, t] (t-major)
-    double (*Bs)[UKP + 4] = reinterpret_cast<double (*)[UKP + 4]>(ub + UKP * UPA2);   // [64][UKP+4] (G S)[j, t]
+__device__ __forceinline__ void cpa8(double* dst, const double* src, bool v) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(v ? 8 : 0));
+}
+__device__ __forceinline__ void cpa16(double* dst, const double* src, int bytes) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(bytes));
+}
+
+__global__ void __launch_bounds__(UT2, 4) k_bigu(DevPlan P, const int2* __restrict__ groups, int ngroups,
+                                                 const int64_t* __restrict__ scroff, double* scr, int* state,
+                                                 unsigned* bars) {
+    extern __shared__ __align__(16) double ubuf[];
+    double (*As)[UKC][UPA2] = reinterpret_cast<double (*)[UKC][UPA2]>(ubuf);                    // G[i, t] (t-major)
+    double (*Bs)[UKC][UPA2] = reinterpret_cast<double (*)[UKC][UPA2]>(ubuf + UST * UKC * UPA2); // G[j, t]
+    __shared__ double sgn[UST][UKC];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, tg = lane & 3;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -393,41 +411,72 @@ __global__ void __launch_bounds__(UT2) k_bigu(DevPlan P, const int2* __restrict_
         double* F = G.F;
         const int nI = (f - e + 63) / 64, nJ = (q - e + 63) / 64;
         const int64_t ntile = (int64_t)nJ * nI - (int64_t)nJ * (nJ - 1) / 2;    // J <= I
+        const int nk = (K + UKC - 1) / UKC;
         for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
-            // tile -> (J, I): column block J holds nI - J tiles
             int J = 0;
             int64_t rem = tile;
             while (rem >= nI - J) { rem -= nI - J; ++J; }
             const int I = J + (int)rem;
             const int i0 = e + 64 * I, j0 = e + 64 * J;
-            __syncthreads();
-            for (int x = tid; x < UKP * 64; x += UT2) {
-                const int t = x >> 6, ii = x & 63;
-                const bool vt = t < K;
-                const int gi = i0 + ii, gj = j0 + ii;
-                As[t][ii] = (vt && gi < f) ? F[gi + (size_t)(k0 + t) * ld] : 0.0;
-                Bs[ii][t] = (vt && gj < q) ? F[gj + (size_t)(k0 + t) * ld] * G.A.sgn[k0 + t] : 0.0;
+            auto load = [&](int buf, int kc) {
+                const int t0 = kc * UKC;
+                for (int x = tid; x < UKC * 32; x += UT2) {           // 16-byte pairs of rows
+                    const int t = x >> 5, r2 = 2 * (x & 31);
+                    const bool vt = t0 + t < K;
+                    const double* ca = F + (size_t)(k0 + t0 + t) * ld;
+                    const int gi = i0 + r2, gj = j0 + r2;
+                    // rows i0.. are even-aligned only when i0 is even: copy pairs when aligned, else singles
+                    if (((i0 & 1) == 0) && ((j0 & 1) == 0)) {
+                        cpa16(&As[buf][t][r2], ca + (vt ? gi : 0), vt ? (gi + 1 < f ? 16 : (gi < f ? 8 : 0)) : 0);
+                        cpa16(&Bs[buf][t][r2], ca + (vt ? gj : 0), vt ? (gj + 1 < q ? 16 : (gj < q ? 8 : 0)) : 0);
+                    } else {
+                        for (int h = 0; h < 2; ++h) {
+                            cpa8(&As[buf][t][r2 + h], ca + (vt && gi + h < f ? gi + h : 0), vt && gi + h < f);
+                            cpa8(&Bs[buf][t][r2 + h], ca + (vt && gj + h < q ? gj + h : 0), vt && gj + h < q);
+                        }
+                    }
+                }
+                if (tid < UKC) sgn[buf][tid] = (t0 + tid < K) ? G.A.sgn[k0 + t0 + tid] : 0.0;
+                asm volatile("cp.async.commit_group;\n" ::);
+            };
+            __syncthreads();                                     // previous tile's smem reads done
+#pragma unroll
+            for (int st0 = 0; st0 < UST - 1; ++st0) {
+                if (st0 < nk) load(st0, st0);
+                else asm volatile("cp.async.commit_group;\n" ::);
             }
-            __syncthreads();
             double acc[4][4][2];
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-            for (int k4 = 0; k4 < K; k4 += 4) {
-                double a[4], b[4];
+            for (int kc = 0; kc < nk; ++kc) {
+                const int buf = kc % UST;
+                asm volatile("cp.async.wait_group %0;\n" ::"n"(UST - 2));
+                __syncthreads();
+                {
+                    const int nx = kc + UST - 1;
+                    if (nx < nk) load(nx % UST, nx);
+                    else asm volatile("cp.async.commit_group;\n" ::);
+                }
 #pragma unroll
-                for (int mb = 0; mb < 4; ++mb) a[mb] = As[k4 + tg][wm + 8 * mb + g];
+                for (int k4 = 0; k4 < UKC; k4 += 4) {
+                    double a[4], b[4];
+                    const double sg = sgn[buf][k4 + tg];
 #pragma unroll
-                for (int nb = 0; nb < 4; ++nb) b[nb] = Bs[wn + 8 * nb + g][k4 + tg];
+                    for (int mb = 0; mb < 4; ++mb) a[mb] = As[buf][k4 + tg][wm + 8 * mb + g];
 #pragma unroll
-                for (int mb = 0; mb < 4; ++mb)
+                    for (int nb = 0; nb < 4; ++nb) b[nb] = Bs[buf][k4 + tg][wn + 8 * nb + g] * sg;
 #pragma unroll
-                    for (int nb = 0; nb < 4; ++nb)
-                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                                     : "+d"(acc[mb][nb][0]), "+d"(acc[mb][nb][1])
-                                     : "d"(a[mb]), "d"(b[nb]));
+                    for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+                        for (int nb = 0; nb < 4; ++nb)
+                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                         : "+d"(acc[mb][nb][0]), "+d"(acc[mb][nb][1])
+                                         : "d"(a[mb]), "d"(b[nb]));
+                }
             }
+            asm volatile("cp.async.wait_group 0;\n" ::);
 #pragma unroll
             for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
@@ -501,14 +550,14 @@ void launch_bigfront(const DevPlan& P, const int2* groups, int ngroups, int ncta
                      int* state, unsigned* bars, int qmax, cudaStream_t st) {
     if (ngroups <= 0) return;
     k_biginit<<<ngroups, 256, 0, st>>>(P, groups, scroff, scr, state, bars);
-    const size_t usmem = sizeof(double) * (UKP * UPA2 + 64 * (UKP + 4));
+    const size_t usmem = sizeof(double) * 2 * UST * UKC * UPA2;
     static unsigned long long attr = 0;
     if (first_on_device(attr)) cudaFuncSetAttribute(k_bigu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
     const int nblk = (qmax + BNB - 2) / (BNB - 1) + 1;       // every block eliminates >= BNB - 1 pivots or finishes
     for (int b = 0; b < nblk; ++b) {
         void* args[] = {(void*)&P, (void*)&groups, (void*)&scroff, (void*)&scr, (void*)&state, (void*)&bars};
         cudaLaunchCooperativeKernel((const void*)k_bigp, dim3(ncta, ngroups), dim3(BT), args, 0, st);
-        k_bigu<<<148 * 3, UT2, usmem, st>>>(P, groups, ngroups, scroff, scr, state, bars);
+        k_bigu<<<148 * 4, UT2, usmem, st>>>(P, groups, ngroups, scroff, scr, state, bars);
     }
     k_bigfin<<<dim3(32, ngroups), 256, 0, st>>>(P, groups, scroff, scr, state, bars);
 }
