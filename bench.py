@@ -430,14 +430,19 @@ def main():
     if rank == 0:
         msd = prof["ms"]
         dom = max(msd, key=lambda x: msd[x])
-        sch_t = msd["schur"] / 1e3
-        roof = {"bound": "tensor", "kernel": "k_schur (a4, DMMA f64)",
+        sch_t = (msd["schur"] + msd["schur_tma"]) / 1e3
+        tma_t = msd["schur_tma"] / 1e3
+        roof = {"bound": "tensor", "kernel": "k_schur + k_schur_tma + k_schur_small (a4, DMMA f64, every level)",
                 "achieved": (prof["schur_flops"] / sch_t / 1e12) if sch_t > 0 else None,
                 "peak": peak, "unit": "TFLOP/s",
                 "frac": (prof["schur_flops"] / sch_t / 1e12 / peak) if sch_t > 0 and peak > 0 else None,
                 "traffic": None,
-                "traffic_note": "not measured by this run; ncu DRAM bytes of k_schur are in profiles/",
+                "traffic_note": "not measured by this run; ncu DRAM bytes of the Schur launches are in profiles/",
                 "peak_source": "cuBLAS DGEMM 8192^3 measured live in bench.py (MEASURED_PEAKS.json has no FP64 entry)",
+                "long_k_levels": {"kernel": "k_schur_tma (TMA-fed, levels averaging >= 128 pivots)",
+                                  "achieved": (prof["schur_tma_flops"] / tma_t / 1e12) if tma_t > 0 else None,
+                                  "frac": (prof["schur_tma_flops"] / tma_t / 1e12 / peak) if tma_t > 0 and peak > 0 else None,
+                                  "share_of_schur_flops": prof["schur_tma_flops"] / max(prof["schur_flops"], 1.0)},
                 "kernel_ms": msd, "kernel_launches": prof["launches"], "dominant_by_time": dom,
                 "schur_flops_alg": prof["schur_flops"]}
         launches = int(sum(prof["launches"].values()) + prof["other_launches"])

@@ -99,13 +99,15 @@ enum { KEP_K_ASSEMBLE = 0,   /* a1 + a2: assembly + extend-add */
        KEP_K_CHECK = 5,      /* a3 + a5: full-column threshold tests, inertia, rerun lists, re-assembly of
                                 fronts that failed them */
        KEP_K_FSU = 6,        /* a3: FS x FS trailing update after each pivot block (k_fsu) */
-       KEP_K_NCLASS = 7 };
+       KEP_K_SCHUR_TMA = 7,  /* a4 on the long-K levels: the TMA-fed k_schur_tma (+ k_schur_small) */
+       KEP_K_NCLASS = 8 };
 
 typedef struct {
     double ms[KEP_K_NCLASS];          /* summed CUDA-event time per class (profile = 1 only) */
     int64_t launches[KEP_K_NCLASS];   /* kernel launches per class (always counted) */
     double schur_flops;               /* algorithmic a4 flops p c (c + 1) summed over the fronts
-                                         whose Schur update ran in KEP_K_SCHUR launches */
+                                         whose Schur update ran in KEP_K_SCHUR or KEP_K_SCHUR_TMA launches */
+    double schur_tma_flops;           /* the part of schur_flops in KEP_K_SCHUR_TMA launches */
     double factor_flops;              /* algorithmic flops of all factorisations run (kep_analysis_info.flops each) */
     int64_t shifts;                   /* shifts factorised */
     int64_t other_launches;           /* bookkeeping kernels (stat reset) */

@@ -1025,13 +1025,16 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             }
             if (keep) kep::launch_store(P, keep->plan(), c->d_level_fronts + b, nfl, c->stream);
             if (c->item_cnt[L] || c->small_cnt[L]) {
-                mark(KEP_K_SCHUR, true);
-                if (c->use_tma && c->tma_level[L]) kep::launch_schur_tma(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
+                const bool tma = c->use_tma && c->tma_level[L];
+                const int cls = tma ? KEP_K_SCHUR_TMA : KEP_K_SCHUR;
+                mark(cls, true);
+                if (tma) kep::launch_schur_tma(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
                 else kep::launch_schur(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
                 kep::launch_schur_small(P, c->d_small + c->small_off[L], (int)c->small_cnt[L], m, c->stream);
-                mark(KEP_K_SCHUR, false);
-                c->prof.launches[KEP_K_SCHUR] += (c->item_cnt[L] ? 1 : 0) + (c->small_cnt[L] ? 1 : 0);
+                mark(cls, false);
+                c->prof.launches[cls] += (c->item_cnt[L] ? 1 : 0) + (c->small_cnt[L] ? 1 : 0);
                 c->prof.schur_flops += c->item_flops[L] * m;
+                if (tma) c->prof.schur_tma_flops += c->item_flops[L] * m;
             }
             if (resid)
                 kep::launch_resid(P, keep->plan(), c->d_ritems + c->ritem_off[L], (int)c->ritem_cnt[L], c->d_f0,
@@ -1973,7 +1976,7 @@ kep_status kep_get_fronts(const kep_ctx* c, int64_t* first, int64_t* parent, int
 void kep_destroy(kep_ctx* c) {
     if (!c) return;
     if (getenv("KEP_PROFILE_LEVELS") && !c->lvl_ms.empty()) {
-        fprintf(stderr, "[kep] per-level kernel ms (assemble fs ref schur l21 check fsu) fronts maxf\n");
+        fprintf(stderr, "[kep] per-level kernel ms (assemble fs ref schur l21 check fsu schur_tma) fronts maxf\n");
         for (size_t L = 0; L < c->lvl_ms.size(); ++L) {
             int mx = 0;
             for (int x = c->sym.level_ptr[L]; x < c->sym.level_ptr[L + 1]; ++x) mx = std::max(mx, (int)c->sym.forder[c->sym.level_fronts[x]]);

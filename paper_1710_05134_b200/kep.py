@@ -35,11 +35,12 @@ class _Opts(C.Structure):
 
 
 class _Profile(C.Structure):
-    _fields_ = [("ms", C.c_double * 7), ("launches", C.c_int64 * 7), ("schur_flops", C.c_double),
-                ("factor_flops", C.c_double), ("shifts", C.c_int64), ("other_launches", C.c_int64)]
+    _fields_ = [("ms", C.c_double * 8), ("launches", C.c_int64 * 8), ("schur_flops", C.c_double),
+                ("schur_tma_flops", C.c_double), ("factor_flops", C.c_double), ("shifts", C.c_int64),
+                ("other_launches", C.c_int64)]
 
 
-KERNEL_CLASSES = ("assemble", "fs", "ref", "schur", "l21", "check", "fsu")
+KERNEL_CLASSES = ("assemble", "fs", "ref", "schur", "l21", "check", "fsu", "schur_tma")
 
 
 class _Info(C.Structure):
@@ -259,7 +260,8 @@ class Kep:
         self._check(lib().kep_get_profile(self._h, C.byref(pr)))
         return dict(ms={n: pr.ms[i] for i, n in enumerate(KERNEL_CLASSES)},
                     launches={n: pr.launches[i] for i, n in enumerate(KERNEL_CLASSES)},
-                    schur_flops=pr.schur_flops, factor_flops=pr.factor_flops, shifts=pr.shifts,
+                    schur_flops=pr.schur_flops, schur_tma_flops=pr.schur_tma_flops, factor_flops=pr.factor_flops,
+                    shifts=pr.shifts,
                     other_launches=pr.other_launches)
 
     def reset_profile(self):

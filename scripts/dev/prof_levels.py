@@ -52,7 +52,8 @@ def main():
     print(f"{m * reps / dt:.3f} shifts/s wall ({dt / reps * 1e3:.1f} ms per {m} shifts); redo/shift "
           f"{np.mean([i.n_redo for i in infos]):.1f} delayed/shift {np.mean([i.n_delayed for i in infos]):.1f}")
     print({kk: round(v / reps, 2) for kk, v in pr["ms"].items()}, "launches", {kk: v // reps for kk, v in pr["launches"].items()})
-    print("schur TF/s", pr["schur_flops"] / (pr["ms"]["schur"] / 1e3) / 1e12)
+    print("schur TF/s", pr["schur_flops"] / ((pr["ms"]["schur"] + pr["ms"]["schur_tma"]) / 1e3) / 1e12,
+          "long-K (tma) TF/s", pr["schur_tma_flops"] / max(pr["ms"]["schur_tma"] / 1e3, 1e-9) / 1e12)
     k.close()
 
 
