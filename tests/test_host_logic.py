@@ -42,3 +42,23 @@ def test_tridiag_eigen_vs_lapack(case):
     if case == 3:                                                        # 2 - 2 cos(pi j / (n + 1))
         j = np.arange(1, n + 1)
         assert np.allclose(w, 2 - 2 * np.cos(np.pi * j / (n + 1)), atol=1e-14, rtol=0)
+
+
+def test_bench_config_identical_in_both_arms():
+    """bench.py prints the same `config` object in the GPU arm and the reference arm (the driver
+    compares them), and it names the BASELINE c4 workload."""
+    import bench
+    a = bench.workload_config(4, None, 1, 16)
+    b = bench.workload_config(4, None, 1, 16)
+    assert a == b and a["workload"] == "c4" and a["n"] == 1_500_000 and a["shifts_per_step"] == 16
+    assert bench.workload_config(4, None, 8, 16)["shifts_per_step"] == 128       # BASELINE: 16 per GPU at 8
+
+
+def test_oracle_flops_golden_consistent():
+    """The CPU-baseline scale factors come from the oracle's own flop counts (scripts/oracle_flops.py)."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_flops.json")))["c4"]
+    assert g["full"] > g["10x10x150"] > g["10x10x100"] > 0
+    # the wire is uniform along z: the per-length cost of the two samples agrees within 15 %
+    assert abs(g["10x10x150"] / 150 - g["10x10x100"] / 100) < 0.15 * g["10x10x100"] / 100
