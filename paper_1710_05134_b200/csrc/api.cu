@@ -898,12 +898,24 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             if (c->big_nf[L] > 0) {                          // large fronts, all SMs (kernels_big.cu)
                 const int ng = (int)(c->big_nf[L] * m);
                 const int ncta = std::max(1, std::min(148 / ng, kBigGroups));
-                mark(KEP_K_PANEL, true);
-                kep::launch_bigfront(P, c->d_big_groups + c->big_goff[L], ng, ncta, c->d_big_scroff + c->big_goff[L],
-                                     c->d_big_scr, c->d_big_state + 16 * c->big_goff[L],
-                                     c->d_big_bars + c->big_goff[L], c->big_qmax[L], c->stream);
-                mark(KEP_K_PANEL, false);
-                c->prof.launches[KEP_K_PANEL] += 2 + 2 * ((c->big_qmax[L] + kep::big_block() - 2) / (kep::big_block() - 1) + 1);
+                const int2* gp = c->d_big_groups + c->big_goff[L];
+                const int64_t* so = c->d_big_scroff + c->big_goff[L];
+                int* sp = c->d_big_state + 16 * c->big_goff[L];
+                unsigned* bp = c->d_big_bars + c->big_goff[L];
+                kep::launch_big_init(P, gp, ng, so, c->d_big_scr, sp, bp, c->stream);
+                const int nblk = kep::big_blocks(c->big_qmax[L]);
+                for (int blk = 0; blk < nblk; ++blk) {
+                    mark(KEP_K_PANEL, true);
+                    kep::launch_big_panel(P, gp, ng, ncta, so, c->d_big_scr, sp, bp, c->stream);
+                    mark(KEP_K_PANEL, false);
+                    mark(KEP_K_FSU, true);                   // the FS trailing update (DMMA, K = 128)
+                    kep::launch_big_update(P, gp, ng, so, c->d_big_scr, sp, bp, c->stream);
+                    mark(KEP_K_FSU, false);
+                }
+                kep::launch_big_fin(P, gp, ng, so, c->d_big_scr, sp, bp, c->stream);
+                c->prof.launches[KEP_K_PANEL] += nblk;
+                c->prof.launches[KEP_K_FSU] += nblk;
+                c->prof.other_launches += 2;
             }
             for (const auto& g : c->sm_groups[L]) {         // whole-panel fronts; overflow -> unblocked kernel
                 mark(KEP_K_PANEL, true);

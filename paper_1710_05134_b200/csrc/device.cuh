@@ -231,8 +231,15 @@ void launch_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batc
 // kernels_big.cu: multi-CTA partial LDL^T of the large fronts of the top levels
 int big_block();
 size_t big_scratch_doubles(int cap, int ncta);
-void launch_bigfront(const DevPlan& P, const int2* groups, int ngroups, int ncta, const int64_t* scroff, double* scr,
-                     int* state, unsigned* bars, int qmax, cudaStream_t st);
+int big_blocks(int qmax);        // k_bigp launches that finish every group of FS capacity <= qmax
+void launch_big_init(const DevPlan& P, const int2* groups, int ngroups, const int64_t* scroff, double* scr, int* state,
+                     unsigned* bars, cudaStream_t st);
+void launch_big_panel(const DevPlan& P, const int2* groups, int ngroups, int ncta, const int64_t* scroff, double* scr,
+                      int* state, unsigned* bars, cudaStream_t st);
+void launch_big_update(const DevPlan& P, const int2* groups, int ngroups, const int64_t* scroff, double* scr,
+                       int* state, unsigned* bars, cudaStream_t st);
+void launch_big_fin(const DevPlan& P, const int2* groups, int ngroups, const int64_t* scroff, double* scr, int* state,
+                    unsigned* bars, cudaStream_t st);
 void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t st);
 void launch_reset_stats(ShiftStat* st, int batch, cudaStream_t s);
 

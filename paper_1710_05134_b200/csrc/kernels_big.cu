@@ -546,19 +546,33 @@ __global__ void k_bigfin(DevPlan P, const int2* __restrict__ groups, const int64
 int big_block() { return BNB; }
 size_t big_scratch_doubles(int cap, int ncta) { return 2 * (size_t)cap + 2 * (size_t)ncta * (sizeof(Part) / 8) + 8; }
 
-void launch_bigfront(const DevPlan& P, const int2* groups, int ngroups, int ncta, const int64_t* scroff, double* scr,
-                     int* state, unsigned* bars, int qmax, cudaStream_t st) {
+void launch_big_init(const DevPlan& P, const int2* groups, int ngroups, const int64_t* scroff, double* scr, int* state,
+                     unsigned* bars, cudaStream_t st) {
     if (ngroups <= 0) return;
     k_biginit<<<ngroups, 256, 0, st>>>(P, groups, scroff, scr, state, bars);
+}
+
+int big_blocks(int qmax) { return (qmax + BNB - 2) / (BNB - 1) + 1; }   // each block eliminates >= BNB - 1 or finishes
+
+void launch_big_panel(const DevPlan& P, const int2* groups, int ngroups, int ncta, const int64_t* scroff, double* scr,
+                      int* state, unsigned* bars, cudaStream_t st) {
+    if (ngroups <= 0) return;
+    void* args[] = {(void*)&P, (void*)&groups, (void*)&scroff, (void*)&scr, (void*)&state, (void*)&bars};
+    cudaLaunchCooperativeKernel((const void*)k_bigp, dim3(ncta, ngroups), dim3(BT), args, 0, st);
+}
+
+void launch_big_update(const DevPlan& P, const int2* groups, int ngroups, const int64_t* scroff, double* scr,
+                       int* state, unsigned* bars, cudaStream_t st) {
+    if (ngroups <= 0) return;
     const size_t usmem = sizeof(double) * 2 * UST * UKC * UPA2;
     static unsigned long long attr = 0;
     if (first_on_device(attr)) cudaFuncSetAttribute(k_bigu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
-    const int nblk = (qmax + BNB - 2) / (BNB - 1) + 1;       // every block eliminates >= BNB - 1 pivots or finishes
-    for (int b = 0; b < nblk; ++b) {
-        void* args[] = {(void*)&P, (void*)&groups, (void*)&scroff, (void*)&scr, (void*)&state, (void*)&bars};
-        cudaLaunchCooperativeKernel((const void*)k_bigp, dim3(ncta, ngroups), dim3(BT), args, 0, st);
-        k_bigu<<<148 * 4, UT2, usmem, st>>>(P, groups, ngroups, scroff, scr, state, bars);
-    }
+    k_bigu<<<148 * 4, UT2, usmem, st>>>(P, groups, ngroups, scroff, scr, state, bars);
+}
+
+void launch_big_fin(const DevPlan& P, const int2* groups, int ngroups, const int64_t* scroff, double* scr, int* state,
+                    unsigned* bars, cudaStream_t st) {
+    if (ngroups <= 0) return;
     k_bigfin<<<dim3(32, ngroups), 256, 0, st>>>(P, groups, scroff, scr, state, bars);
 }
 
