@@ -45,6 +45,7 @@ from .dense_bk import ALPHA, Inertia, block_inertia_1x1, block_inertia_2x2
 
 U_THRESHOLD = 0.01
 LEAF = 16
+_CHUNK = 2048           # column chunk of the blocked path's large products (bounds temporaries only)
 
 
 # ----------------------------------------------------------------------------- ordering
@@ -223,7 +224,10 @@ class SparseOracle:
                 cidx, C = cbs.pop(c)
                 li = pos[np.asarray(cidx)]
                 assert np.all(li >= 0)
-                F[np.ix_(li, li)] += C
+                for j0 in range(0, li.shape[0], _CHUNK):    # column chunks (memory only)
+                    j1 = min(li.shape[0], j0 + _CHUNK)
+                    F[np.ix_(li, li[j0:j1])] += C[:, j0:j1]
+                del C
             root = rest.shape[0] == 0
             if nb > 0:
                 inert, order, e_cnt = _partial_fs_bk_blocked(F, fs.shape[0], u=u, root=root, nb=nb)
@@ -232,8 +236,9 @@ class SparseOracle:
             total.add(inert)
             if not root:
                 loc = order[e_cnt:]
-                cbs[b] = (idx[loc].tolist(), F[e_cnt:, e_cnt:])
+                cbs[b] = (idx[loc].tolist(), np.array(F[e_cnt:, e_cnt:], order="F"))   # a copy: F is freed
             pos[idx] = -1
+            del F
         return total
 
 
@@ -404,7 +409,9 @@ def _partial_fs_bk_blocked(F: np.ndarray, nfs: int, u: float, root: bool, nb: in
     def flush():
         nonlocal t
         if t and e < q:
-            F[e:, e:q] -= Lp[e:, :t] @ Wp[e:q, :t].T
+            for j0 in range(e, q, _CHUNK):          # column chunks: bounded temporaries (memory only)
+                j1 = min(q, j0 + _CHUNK)
+                F[e:, j0:j1] -= Lp[e:, :t] @ Wp[j0:j1, :t].T
         t = 0
 
     while e < qe:
@@ -510,11 +517,16 @@ def _partial_fs_bk_blocked(F: np.ndarray, nfs: int, u: float, root: bool, nb: in
         W = np.zeros_like(L)
         for (k, sz, Dk) in Dblocks:
             W[:, k:k + sz] = L[:, k:k + sz] @ Dk
-        F[q:, q:] -= W @ L.T
-    if e < f:
-        T = F[e:, e:]
-        lowT = np.tril(T)
-        F[e:, e:] = lowT + np.tril(lowT, -1).T
+        for j0 in range(q, f, _CHUNK):              # column chunks (memory only)
+            j1 = min(f, j0 + _CHUNK)
+            F[q:, j0:j1] -= W @ L[j0 - q:j1 - q].T
+    if e < f:                                       # symmetric trailing block: upper <- lower, in place
+        for j0 in range(e, f, _CHUNK):
+            j1 = min(f, j0 + _CHUNK)
+            B = F[j0:j1, j0:j1]
+            B[:] = np.tril(B) + np.tril(B, -1).T
+            if j1 < f:
+                F[j0:j1, j1:] = F[j1:, j0:j1].T
     return res, order, e
 
 
