@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
             if (t == skip) continue;
             double* x = F + a + (size_t)t * ld;
             double* y = F + b + (size_t)t * ld;
-            const double v = *x; *x = *y; *y = v;
+            const double vx = __ldcg(x), vy = __ldcg(y);            // rows owned by other CTAs: via L2
+            *x = vy; *y = vx;
         }
         for (int i = max(ra, a + 1) + tid; i < rb; i += BT) {
             if (i == b) continue;
@@ -200,12 +201,14 @@ __global__ void __launch_bounds__(BT, 1) k_bigp(DevPlan P, const int2* __restric
     auto column = [&](int j, int k, double* out) {
         const int nt = k - k0;
         __syncthreads();
-        for (int t = tid; t < nt; t += BT) sG[t] = F[j + (size_t)(k0 + t) * ld] * A.sgn[k0 + t];
+        // F is read through L2 (ld.global.cg): other CTAs of the group wrote it (G columns, interchanges)
+        // before the last group barrier, and L1 lines cached earlier would be stale
+        for (int t = tid; t < nt; t += BT) sG[t] = __ldcg(F + j + (size_t)(k0 + t) * ld) * __ldcg(A.sgn + k0 + t);
         __syncthreads();
         for (int i = max(ra, k) + tid; i < rb; i += BT) {
-            double v = i >= j ? F[i + (size_t)j * ld] : F[j + (size_t)i * ld];
+            double v = i >= j ? __ldcg(F + i + (size_t)j * ld) : __ldcg(F + j + (size_t)i * ld);
             const double* gi = F + i + (size_t)k0 * ld;
-            for (int t = 0; t < nt; ++t) v = fma(-gi[(size_t)t * ld], sG[t], v);
+            for (int t = 0; t < nt; ++t) v = fma(-__ldcg(gi + (size_t)t * ld), sG[t], v);
             out[i] = v;
         }
         __syncthreads();                            // the column's own rows are read by other threads next
