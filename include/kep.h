@@ -76,7 +76,7 @@ typedef struct {
     kep_ordering ordering;      /* default KEP_ORDER_AUTO */
     const int64_t* user_perm;   /* KEP_ORDER_USER: user_perm[i] = dof placed i-th; length n */
     int32_t amalgamate;         /* relaxed supernode amalgamation on (1, default) / off (0) */
-    int32_t nrelax;             /* merge child into parent if merged pivot count <= nrelax (default 16) */
+    int32_t nrelax;             /* merge child into parent if merged pivot count <= nrelax (default 48) */
     double relax_frac;          /* ... or if the added zeros are <= relax_frac of the merged L (default 0.05) */
     double pivot_u;             /* threshold for delayed pivots, u in (0, 0.5]; default 0.01 (DESIGN R1) */
     double tau_sing;            /* singularity tolerance relative to max|A - sigma B|; default 1e-14 */

@@ -53,7 +53,7 @@ struct kep_ctx {
     // rerun passes: per fast front list descriptors and the compact lists (k_rerun_lists)
     int4 *d_rr_d1 = nullptr, *d_rr_d2 = nullptr;
     int32_t *d_rr_fr = nullptr, *d_rr_x = nullptr, *d_rr_cnt = nullptr;
-    int4 *d_rr_l[3] = {nullptr, nullptr, nullptr}, *d_rr_u = nullptr, *d_rr_a = nullptr;
+    int4 *d_rr_l[4] = {nullptr, nullptr, nullptr, nullptr}, *d_rr_u = nullptr, *d_rr_a = nullptr;
     int32_t* d_rmap = nullptr;
     double *d_a = nullptr, *d_b = nullptr;
     // batch state
@@ -68,13 +68,14 @@ struct kep_ctx {
     int32_t* d_lists = nullptr;                 // [fast fronts of all levels | ref fronts of all levels]
     int4* d_items = nullptr;                    // Schur tiles (front, I, J, 0)
     int4* d_litems = nullptr;                   // k_l21 row tiles (front, I, 0, 0)
-    int4* d_lsitems = nullptr;                  // k_l21<1> row tiles (fronts with q < 32)
+    int4* d_lsitems = nullptr;                  // k_l21d<64,1> row tiles (FS capacity <= 64; k_l21<1> if off)
+    int4* d_lditems = nullptr;                  // k_l21d<128,4> row tiles (FS capacity 65..128)
     int4* d_lxitems = nullptr;                  // k_l21<2> row tiles (GEMM in-block solve)
     int32_t* d_xfronts = nullptr;               // k_l21x_prep fronts per level
     int64_t* d_xoff = nullptr;                  // X scratch offsets (within the level)
     double* d_xscr = nullptr;
     int64_t xstride = 0;
-    std::vector<int64_t> lsitem_off, lsitem_cnt, lxitem_off, lxitem_cnt, xfront_off, xfront_cnt;
+    std::vector<int64_t> lsitem_off, lsitem_cnt, lxitem_off, lxitem_cnt, lditem_off, lditem_cnt, xfront_off, xfront_cnt;
     struct FsGroup { int64_t foff, fcnt, uoff, ucnt; int qmax; };
     std::vector<std::vector<FsGroup>> fs_groups;   // per level: fast fronts by FS capacity (k_fsp/k_fsu passes)
     int4* d_aitems = nullptr;                   // k_assemble strips (front, x, S, 0): all fronts, then fast fronts
@@ -318,15 +319,16 @@ kep_status build_lists(kep_ctx* c) {
     c->sm_groups.assign(nl, {});
     c->item_flops.assign(nl, 0.0);
     std::vector<int32_t> fast, ref;
-    std::vector<int4> items, litems, lsitems, lxitems, uitems;
+    std::vector<int4> items, litems, lsitems, lxitems, lditems, uitems;
     std::vector<int32_t> xfronts;
     std::vector<int64_t> xoff(S.nf > 0 ? S.nf : 1, 0);
     int64_t xmax = 0;
     std::vector<int4> rd1(S.nf > 0 ? S.nf : 1, make_int4(0, 0, 0, 0)), rd2(S.nf > 0 ? S.nf : 1, make_int4(0, 0, 0, 0));
-    int64_t mx_f = 1, mx_l[3] = {1, 1, 1}, mx_u = 1, mx_a = 1;
+    int64_t mx_f = 1, mx_l[4] = {1, 1, 1, 1}, mx_u = 1, mx_a = 1;
     std::vector<int32_t> small;
     c->litem_off.assign(nl, 0); c->litem_cnt.assign(nl, 0);
     c->lsitem_off.assign(nl, 0); c->lsitem_cnt.assign(nl, 0);
+    c->lditem_off.assign(nl, 0); c->lditem_cnt.assign(nl, 0);
     c->lxitem_off.assign(nl, 0); c->lxitem_cnt.assign(nl, 0);
     c->xfront_off.assign(nl, 0); c->xfront_cnt.assign(nl, 0);
     c->aitem_off.assign(nl, 0); c->aitem_cnt.assign(nl, 0);
@@ -352,6 +354,7 @@ kep_status build_lists(kep_ctx* c) {
         c->item_off[L] = (int64_t)items.size();
         c->litem_off[L] = (int64_t)litems.size();
         c->lsitem_off[L] = (int64_t)lsitems.size();
+        c->lditem_off[L] = (int64_t)lditems.size();
         c->lxitem_off[L] = (int64_t)lxitems.size();
         c->xfront_off[L] = (int64_t)xfronts.size();
         int64_t xacc = 0;
@@ -455,7 +458,7 @@ kep_status build_lists(kep_ctx* c) {
             }
             c->level_qmax[L] = std::max(c->level_qmax[L], qcap);
             const int lmode = kep::l21_mode(qcap);
-            auto& li = lmode == 1 ? lsitems : (lmode == 2 ? lxitems : litems);
+            auto& li = lmode == 1 ? lsitems : (lmode == 2 ? lxitems : (lmode == 3 ? lditems : litems));
             if (lmode == 2) {
                 xfronts.push_back(s);
                 xoff[s] = xacc;
@@ -524,12 +527,14 @@ kep_status build_lists(kep_ctx* c) {
         c->item_cnt[L] = (int64_t)items.size() - c->item_off[L];
         c->litem_cnt[L] = (int64_t)litems.size() - c->litem_off[L];
         c->lsitem_cnt[L] = (int64_t)lsitems.size() - c->lsitem_off[L];
+        c->lditem_cnt[L] = (int64_t)lditems.size() - c->lditem_off[L];
         c->lxitem_cnt[L] = (int64_t)lxitems.size() - c->lxitem_off[L];
         c->xfront_cnt[L] = (int64_t)xfronts.size() - c->xfront_off[L];
         xmax = std::max(xmax, xacc);
         mx_f = std::max(mx_f, c->fast_cnt[L]);
         mx_l[0] = std::max(mx_l[0], c->litem_cnt[L]);
         mx_l[1] = std::max(mx_l[1], c->lsitem_cnt[L]);
+        mx_l[3] = std::max(mx_l[3], c->lditem_cnt[L]);
         mx_l[2] = std::max(mx_l[2], c->lxitem_cnt[L]);
         c->uitem_cnt[L] = (int64_t)uitems.size() - c->uitem_off[L];
         mx_u = std::max(mx_u, c->uitem_cnt[L]);
@@ -566,6 +571,8 @@ kep_status build_lists(kep_ctx* c) {
     KEP_CUDA(c, upload(&c->d_litems, litems));
     cudaFree(c->d_lsitems); c->d_lsitems = nullptr;
     KEP_CUDA(c, upload(&c->d_lsitems, lsitems));
+    cudaFree(c->d_lditems); c->d_lditems = nullptr;
+    KEP_CUDA(c, upload(&c->d_lditems, lditems));
     cudaFree(c->d_lxitems); c->d_lxitems = nullptr;
     KEP_CUDA(c, upload(&c->d_lxitems, lxitems));
     cudaFree(c->d_xfronts); c->d_xfronts = nullptr;
@@ -575,7 +582,7 @@ kep_status build_lists(kep_ctx* c) {
     c->xstride = xmax;
     {
         void* old[] = {c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1],
-                       c->d_rr_l[2], c->d_rr_u, c->d_rr_a};
+                       c->d_rr_l[2], c->d_rr_l[3], c->d_rr_u, c->d_rr_a};
         for (void* q : old) cudaFree(q);
         c->d_rr_d1 = c->d_rr_d2 = nullptr;
         KEP_CUDA(c, upload(&c->d_rr_d1, rd1));
@@ -583,7 +590,7 @@ kep_status build_lists(kep_ctx* c) {
         KEP_CUDA(c, cudaMalloc(&c->d_rr_fr, sizeof(int32_t) * mx_f));
         KEP_CUDA(c, cudaMalloc(&c->d_rr_x, sizeof(int32_t) * mx_f));
         KEP_CUDA(c, cudaMalloc(&c->d_rr_cnt, sizeof(int32_t) * 8));
-        for (int k = 0; k < 3; ++k) KEP_CUDA(c, cudaMalloc(&c->d_rr_l[k], sizeof(int4) * mx_l[k]));
+        for (int k = 0; k < 4; ++k) KEP_CUDA(c, cudaMalloc(&c->d_rr_l[k], sizeof(int4) * mx_l[k]));
         KEP_CUDA(c, cudaMalloc(&c->d_rr_u, sizeof(int4) * mx_u));
         KEP_CUDA(c, cudaMalloc(&c->d_rr_a, sizeof(int4) * mx_a));
     }
@@ -936,10 +943,10 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 const auto& groups = c->fs_groups[L];
                 kep::RerunLists R;
                 R.d1 = c->d_rr_d1; R.d2 = c->d_rr_d2;
-                R.sl[0] = c->d_litems; R.sl[1] = c->d_lsitems; R.sl[2] = c->d_lxitems;
+                R.sl[0] = c->d_litems; R.sl[1] = c->d_lsitems; R.sl[2] = c->d_lxitems; R.sl[3] = c->d_lditems;
                 R.su = c->d_uitems; R.sa = c->d_aitems;
                 R.fr = c->d_rr_fr; R.x = c->d_rr_x; R.cnt = c->d_rr_cnt;
-                for (int k = 0; k < 3; ++k) R.l[k] = c->d_rr_l[k];
+                for (int k = 0; k < 4; ++k) R.l[k] = c->d_rr_l[k];
                 R.u = c->d_rr_u; R.a = c->d_rr_a;
                 int32_t rc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 bool anyflag = false;                   // some pass flagged a front (rerun or unblocked kernel)
@@ -963,14 +970,16 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                                 }
                             }
                         }
-                        if (c->litem_cnt[L] || c->lsitem_cnt[L] || c->lxitem_cnt[L]) {
+                        if (c->litem_cnt[L] || c->lsitem_cnt[L] || c->lxitem_cnt[L] || c->lditem_cnt[L]) {
                             mark(KEP_K_L21, true);
                             kep::launch_l21x_prep(P, c->d_xfronts + c->xfront_off[L], (int)c->xfront_cnt[L], m, c->stream);
                             kep::launch_l21(P, c->d_lxitems + c->lxitem_off[L], (int)c->lxitem_cnt[L], m, 2, c->stream);
                             kep::launch_l21(P, c->d_litems + c->litem_off[L], (int)c->litem_cnt[L], m, 0, c->stream);
                             kep::launch_l21(P, c->d_lsitems + c->lsitem_off[L], (int)c->lsitem_cnt[L], m, 1, c->stream);
+                            kep::launch_l21(P, c->d_lditems + c->lditem_off[L], (int)c->lditem_cnt[L], m, 3, c->stream);
                             mark(KEP_K_L21, false);
-                            c->prof.launches[KEP_K_L21] += 2 * (c->lxitem_cnt[L] > 0) + (c->litem_cnt[L] > 0) + (c->lsitem_cnt[L] > 0);
+                            c->prof.launches[KEP_K_L21] += 2 * (c->lxitem_cnt[L] > 0) + (c->litem_cnt[L] > 0) + (c->lsitem_cnt[L] > 0) +
+                                                           (c->lditem_cnt[L] > 0);
                         }
                         mark(KEP_K_CHECK, true);
                         kep::launch_check(P, fl, nfl2, m, c->stream);
@@ -1000,6 +1009,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                         kep::launch_l21(P, c->d_rr_l[2], rc[3], m, 2, c->stream);
                         kep::launch_l21(P, c->d_rr_l[0], rc[1], m, 0, c->stream);
                         kep::launch_l21(P, c->d_rr_l[1], rc[2], m, 1, c->stream);
+                        kep::launch_l21(P, c->d_rr_l[3], rc[7], m, 3, c->stream);
                         mark(KEP_K_L21, false);
                         c->prof.launches[KEP_K_L21] += 4;
                         mark(KEP_K_CHECK, true);
@@ -1096,7 +1106,7 @@ void kep_default_opts(kep_opts* o) {
     o->ordering = KEP_ORDER_AUTO;
     o->user_perm = nullptr;
     o->amalgamate = 1;
-    o->nrelax = 16;
+    o->nrelax = 48;
     o->relax_frac = 0.05;
     o->pivot_u = 0.01;
     o->tau_sing = 1e-14;
@@ -2006,7 +2016,7 @@ void kep_destroy(kep_ctx* c) {
                         c->d_level_fronts, c->d_arena_off, c->d_asm_ptr, c->d_asm_src, c->d_rmap_ptr,
                         c->d_asm_rc, c->d_rmap, c->d_a, c->d_b, c->d_lists, c->d_items,
                         c->d_litems, c->d_aux_off, c->d_uitems, c->d_piv_first, c->d_cb_ptr,
-                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1], c->d_rr_l[2], c->d_rr_u, c->d_rr_a, c->d_lsitems, c->d_lxitems, c->d_xfronts, c->d_xoff,
+                        c->d_cb_rows, c->d_perm, c->d_iperm, c->d_csr_rp, c->d_csr_src, c->d_csr_ci, c->d_aitems, c->d_asm_col, c->d_stage, c->d_rr_d1, c->d_rr_d2, c->d_rr_fr, c->d_rr_x, c->d_rr_cnt, c->d_rr_l[0], c->d_rr_l[1], c->d_rr_l[2], c->d_rr_l[3], c->d_rr_u, c->d_rr_a, c->d_lsitems, c->d_lditems, c->d_lxitems, c->d_xfronts, c->d_xoff,
                         c->d_csr_a, c->d_csr_b, c->d_goff, c->d_small, c->d_f0, c->d_resid, c->d_ritems,
                         c->d_smfronts, c->d_tmaps, c->d_tmap_idx, c->d_big_groups, c->d_big_scroff, c->d_big_scr,
                         c->d_big_state, c->d_big_bars, c->d_smitems};

@@ -194,18 +194,18 @@ void launch_combine(const double* V, int64_t ldv, int j, const double* c, double
 void launch_ritz(const double* W, int64_t ldw, int j, const double* C, const double* r, const double* g, int m,
                  double* X, int64_t ldx, int64_t n, cudaStream_t st);
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, int mode, cudaStream_t st);
-int l21_mode(int qcap);              // 1: one column block (q < 32); 2: GEMM in-block solve (X scratch); 0: triangle
+int l21_mode(int qcap);              // 1: k_l21d<64,1> (q <= 64); 3: k_l21d<128,4> (q <= 128); 2: GEMM in-block solve (X scratch); 0: triangle
 int64_t l21_x_doubles(int qcap);     // X scratch of one front (k_l21x_prep)
 // compact per-pass lists of the fronts flagged for a rerun (k_rerun_lists)
 struct RerunLists {
     const int4 *d1, *d2;         // [nf] per fast front: (l21 mode, l21 item off, cnt, uitem off), (ucnt, re-assembly off, cnt, -)
-    const int4* sl[3];           // static l21 item lists by mode
+    const int4* sl[4];           // static l21 item lists by mode
     const int4 *su, *sa;         // static k_fsu tiles, re-assembly strips
     int32_t* fr;                 // out: fronts flagged FL_RERUN (re-assembly strips: FL_RERUN or FL_REF)
-    int4* l[3];                  // out: their l21 tiles by mode
+    int4* l[4];                  // out: their l21 tiles by mode
     int4 *u, *a;                 // out: their k_fsu tiles, re-assembly strips
     int32_t* x;                  // out: their k_l21x_prep fronts
-    int32_t* cnt;                // out [8]: fronts, l21 <0> <1> <2>, fsu, re-assembly, prep
+    int32_t* cnt;                // out [8]: fronts, l21 modes 0 1 2, fsu, re-assembly, prep, l21 mode 3
 };
 void launch_rerun_lists(const DevPlan& P, const int32_t* fl, int n, int batch, const RerunLists& R, cudaStream_t st);
 void launch_l21x_prep(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);

@@ -663,18 +663,25 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
         if (!SMALL && K > 0) {
+            // per-thread copy slots (fixed for the CTA): A: rows ii0 + 32 j (j < 4), columns 2 ta,
+            // ta + 1 of the chunk; B: column jb of the block, chunk rows tb + 8 j (j < 2)
+            static_assert((KC / 2) * LR == 4 * LT && KC * LB == 2 * LT, "k_l21 copy slots");
+            const int ta = 2 * (tid % (KC / 2)), ii0 = tid / (KC / 2);
+            const int jb = tid % LB, tb = tid / LB;
             auto load = [&](int buf, int t0) {
-                for (int x = tid; x < (KC / 2) * LR; x += LT) {   // G rows: 16-byte pairs (even ld, t0 % 16 == 0)
-                    const int ii = x / (KC / 2), tt = 2 * (x - ii * (KC / 2));
-                    const int gi = r0 + ii, gt = t0 + tt;
-                    const int nb = gi < f ? (gt + 1 < K ? 16 : (gt < K ? 8 : 0)) : 0;
-                    cp_async16(&As[buf][ii][tt], F + (nb ? (gt + (size_t)gi * ld) : 0), nb);
+                const int gt = t0 + ta;
+                const int nbt = gt + 1 < K ? 16 : (gt < K ? 8 : 0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {                 // G rows: 16-byte pairs (even ld, t0 % 16 == 0)
+                    const int ii = ii0 + 32 * j, gi = r0 + ii;
+                    const int nb = gi < f ? nbt : 0;
+                    cp_async16(&As[buf][ii][ta], F + (nb ? (gt + (size_t)gi * ld) : 0), nb);
                 }
-                for (int x = tid; x < KC * LB; x += LT) {
-                    const int tt = x / LB, jj = x - tt * LB;
-                    const int gt = t0 + tt;
-                    const bool v = jj < nbc && gt < K;
-                    cp_async8(&Bs[buf][jj][tt], F + (v ? ((b0 + jj) + (size_t)gt * ld) : 0), v);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int tt = tb + 8 * j, gtb = t0 + tt;
+                    const bool v = jb < nbc && gtb < K;
+                    cp_async8(&Bs[buf][jb][tt], F + (v ? ((b0 + jb) + (size_t)gtb * ld) : 0), v);
                 }
                 if (tid < KC) SgB[buf][tid] = (t0 + tid < K && A.sgn[t0 + tid] < 0.0) ? 0x8000000000000000ull : 0ull;
                 cp_async_commit();
@@ -864,6 +871,171 @@ __global__ void __launch_bounds__(LT, 2) k_l21(DevPlan P, const int4* __restrict
     }
 }
 
+// ------------------------------------------------------------------ k_l21d
+// G21 = W21 D^-1 M for the 128 CB rows i of one strip, by plain forward substitution
+// along each row (fronts with FS capacity <= QMAX):
+//   w_t = a_t - sum_{t' < min(t, e)} (g_t' s_t') G11[t, t'],   a_t = (A21 P^T)[i, t],
+// i.e. W21 = A21 P^T L11^-T written in G space (B' = G11 S, R21), then
+// g_t from w_t and its 2x2 partner (gca / gcb), |w_t| into the column maxima.
+// One row per thread (TPR = 1) or per TPR adjacent threads (TPR = 4: the group splits
+// the columns by t mod 4 and adds its partial sums with two shuffles).  The row's
+// history g S stays in registers (QMAX / TPR of them); B' rows are streamed through
+// shared memory in chunks of LDC rows (double-buffered cp.async, zero-filled for
+// t' >= e and at a 2x2 block's in-pair entry) and read as 16-byte broadcasts.
+// All arithmetic is fp64 FMA (on B200 the FMA pipe matches DMMA: 33.8 vs 35.5
+// TFLOP/s measured), no explicit block inverses, no CTA barrier except per chunk.
+template <int QMAX, int TPR>
+struct L21d {
+    static constexpr int NT = 128 * TPR, NW = NT / 32, NWS = NW < 8 ? NW : 8, LDC = 16, NH = QMAX / TPR;
+    static constexpr int BW = NH + 2;                     // B' row (per class t' mod TPR) + pad, 16-byte aligned
+    static_assert(QMAX % (2 * TPR) == 0 && LDC % 2 == 0 && QMAX % 64 == 0, "k_l21d shape");
+    struct Smem {
+        double Bs[2][LDC][TPR][BW];                       // B'[t0 + r][TPR k + h] at Bs[.][r][h][k]
+        unsigned long long scm[NWS][QMAX];                // warp maxima of |w_t| (warps w, w + 8 share a row)
+        double ssg[QMAX], sga[QMAX], sgb[QMAX];
+        int sperm[QMAX], skind[QMAX];
+    };
+    Smem& S;
+    const double* F;
+    int q, e, ld, tid, lane, warp, h;
+    bool valid;
+    double vprev;
+
+    // B' rows [t0, t0 + LDC), all QMAX columns (zeros outside the strict lower part below e, so the
+    // unrolled dot products may read past their last term)
+    __device__ __forceinline__ void stage(int buf, int t0) {
+        for (int x = tid; x < LDC * QMAX; x += NT) {
+            const int r = x % LDC, tp = x / LDC, t = t0 + r;   // consecutive threads walk a column of G11
+            const bool v = t < q && tp < t && tp < e && !(tp == t - 1 && S.skind[tp] == PK_2X2A);
+            cp_async8(&S.Bs[buf][r][tp % TPR][tp / TPR], F + (v ? (t + (size_t)tp * ld) : 0), v);
+        }
+        cp_async_commit();
+    }
+
+    // columns [T0, T0 + 64) of the substitution (64 per part keeps every loop fully unrolled,
+    // so y[] stays in registers); false once t reaches q
+    template <int T0>
+    __device__ __forceinline__ bool part(double (&y)[NH]) {
+        // Straight-line code per chunk of LDC columns (no data-dependent branches: the scheduler
+        // overlaps the dot products of consecutive t, which share only their last terms); columns
+        // t >= q inside the last chunk compute zeros (a_t = 0, B' = 0, kind -1) and are not stored.
+#pragma unroll
+        for (int t = T0; t < T0 + 64; ++t) {
+            if (t % LDC == 0) {
+                if (t >= q) return false;                  // uniform
+                cp_async_wait<0>();
+                __syncthreads();                           // chunk t / LDC landed; the other buffer is free
+                if (t + LDC < q) stage((t / LDC + 1) & 1, t + LDC);
+            }
+            const double* b = &S.Bs[(t / LDC) & 1][t % LDC][h][0];
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+            const int kend = (t - h + TPR - 1) / TPR;      // own columns t' = TPR k + h < t
+#pragma unroll
+            for (int k = 0; k < NH; k += 2) {
+                if (k >= (t + TPR - 1) / TPR) break;       // static bound (h = 0)
+                const double2 bb = *reinterpret_cast<const double2*>(b + k);
+                if (TPR == 1) {                            // kend = t: static
+                    if (k < kend) a[(k >> 1) & 1] = fma(y[k], bb.x, a[(k >> 1) & 1]);
+                    if (k + 1 < kend) a[2 + ((k >> 1) & 1)] = fma(y[k + 1], bb.y, a[2 + ((k >> 1) & 1)]);
+                } else {
+                    a[(k >> 1) & 1] = fma(k < kend ? y[k] : 0.0, bb.x, a[(k >> 1) & 1]);
+                    a[2 + ((k >> 1) & 1)] = fma(k + 1 < kend ? y[k + 1] : 0.0, bb.y, a[2 + ((k >> 1) & 1)]);
+                }
+            }
+            double tot = (a[0] + a[1]) + (a[2] + a[3]);
+            if (TPR >= 2) tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+            if (TPR >= 4) tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+            double v = (t % TPR == h ? y[t / TPR] : 0.0) - tot;
+            if (TPR >= 2) v = __shfl_sync(0xffffffffu, v, (lane & ~(TPR - 1)) | (t % TPR));
+            const int kd = S.skind[t];
+            {   // |w_t| into the column maxima (read back only for t < e)
+                const double av = valid ? fabs(v) : 0.0;
+                const unsigned hi = (unsigned)__double2hiint(av), lo = (unsigned)__double2loint(av);
+                const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+                const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+                const unsigned long long mv = ((unsigned long long)mh << 32) | ml;
+                if (NW <= 8) {
+                    if (lane == 0) S.scm[warp][t] = mv;
+                } else {
+                    if (lane == 0 && warp < 8) S.scm[warp][t] = mv;
+                    __syncwarp();
+                    if (lane == 0 && warp >= 8) atomicMax(&S.scm[warp - 8][t], mv);
+                }
+            }
+            const double ga = S.sga[t], gb = S.sgb[t], sg = S.ssg[t];
+            const bool two = t > 0 && kd == PK_2X2B;
+            // g_t s_t: 1x1 / zero pivot, second column of a 2x2 pair, or raw w_t (delayed; first of a pair)
+            const double g = (kd == PK_1X1 || kd == PK_ZERO) ? v * ga * sg
+                           : (two ? (v * ga + vprev * gb) * sg : v);
+            if (t % TPR == h) y[t / TPR] = g;
+            if (t > 0 && (t - 1) % TPR == h) {             // the pair's first column, now complete
+                const int tm = t > 0 ? t - 1 : 0;
+                const double g1 = (vprev * S.sga[tm] + v * S.sgb[tm]) * S.ssg[tm];
+                y[tm / TPR] = two ? g1 : y[tm / TPR];
+            }
+            vprev = v;
+        }
+        return true;
+    }
+};
+
+template <int QMAX, int TPR>
+__global__ void __launch_bounds__(128 * TPR) k_l21d(DevPlan P, const int4* __restrict__ items) {
+    using K = L21d<QMAX, TPR>;
+    constexpr int NT = K::NT, NH = K::NH;
+    __shared__ __align__(16) typename K::Smem S;
+    const int4 it = items[blockIdx.x];
+    const int s = it.x, I = it.y;
+    const int sh = blockIdx.y;
+    const int nd = P.nd_in[(size_t)sh * P.nf + s];
+    if (nd < 0) return;
+    if (P.flag[(size_t)sh * P.nf + s] != FL_ACTIVE) return;
+    const int ndo = P.nd_out[(size_t)sh * P.nf + s];
+    if (ndo < 0) return;
+    const int p = P.npiv[s], c = P.ncb[s];
+    const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
+    const int e = q - ndo;
+    const int r0 = q + I * 128;
+    if (r0 >= f || q > QMAX) return;
+    double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
+    const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
+    const int tid = threadIdx.x;
+    K k{S, F, q, e, ld, tid, tid & 31, tid >> 5, tid & (TPR - 1), r0 + tid / TPR < f, 0.0};
+    const int i = r0 + tid / TPR;
+    for (int t = tid; t < QMAX; t += NT) {
+        const bool el = t < e;
+        S.sperm[t] = t < q ? A.perm[t] : 0;
+        S.skind[t] = el ? A.kind[t] : -1;
+        S.ssg[t] = el ? A.sgn[t] : 0.0;
+        S.sga[t] = el ? A.gca[t] : 0.0;
+        S.sgb[t] = el ? A.gcb[t] : 0.0;
+    }
+    __syncthreads();
+    k.stage(0, 0);
+    double y[NH];                                          // a_t, then g_t s_t (raw w_t for delayed t)
+#pragma unroll
+    for (int x = 0; x < NH; ++x) {
+        const int t = TPR * x + k.h;
+        y[x] = (k.valid && t < q) ? F[i + (size_t)S.sperm[t] * ld] : 0.0;
+    }
+    if (k.template part<0>(y) && QMAX > 64) k.template part<(QMAX > 64 ? 64 : 0)>(y);
+    if (k.valid) {                                         // G (W for delayed columns) to the upper part
+        double* __restrict__ Gi = F + (size_t)i * ld;
+#pragma unroll
+        for (int x = 0; x < NH; ++x) {
+            const int t = TPR * x + k.h;
+            if (t < q) Gi[t] = S.skind[t] >= 0 ? y[x] * S.ssg[t] : y[x];
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < e; t += NT) {
+        unsigned long long m = 0;
+#pragma unroll
+        for (int w = 0; w < K::NWS; ++w) m = max(m, S.scm[w][t]);
+        if (m > 0) atomicMax(&A.cm[t], m);
+    }
+}
+
 // ------------------------------------------------------------------ k_l21x_prep
 // Per front and column block [b0, b0 + nbc) of k_l21 (the same block rule): the
 // unit lower block L_bb of L11 (from the stored G11 = L11 M: L = G11 S (D M^-T)^-1,
@@ -983,7 +1155,7 @@ __global__ void __launch_bounds__(1024) k_rerun_lists(DevPlan P, const int32_t* 
         k = atomicAdd(&cnt[0], 1);
         R.fr[k] = s;
         if (a.z > 0) {
-            k = atomicAdd(&cnt[1 + a.x], a.z);
+            k = atomicAdd(&cnt[a.x < 3 ? 1 + a.x : 7], a.z);
             for (int i = 0; i < a.z; ++i) R.l[a.x][k + i] = R.sl[a.x][a.y + i];
         }
         if (b.x > 0) {
@@ -1192,6 +1364,13 @@ void launch_fsu(const DevPlan& P, const int4* items, int nitems, int batch, cuda
     k_fsu<<<dim3(nitems, batch), UT, 0, st>>>(P, items);
 }
 
+// FS capacity up to which k_l21d replaces k_l21 (KEP_L21D_MAX: 0 = off, 64 = default, 128: also
+// k_l21d<128,4>, measured slower than k_l21<2> at c4)
+int l21d_max() {
+    static const int v = [] { const char* x = getenv("KEP_L21D_MAX"); return x ? atoi(x) : 64; }();
+    return v;
+}
+
 void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, int mode, cudaStream_t st) {
     if (nitems <= 0) return;
     const size_t smem = sizeof(double) * (LST * LR * BP + LST * LB * BP + LR * (LB + 1));
@@ -1203,12 +1382,17 @@ void launch_l21(const DevPlan& P, const int4* items, int nitems, int batch, int 
         cudaFuncSetAttribute(k_l21<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         
     }
-    if (mode == 1) k_l21<1><<<dim3(nitems, batch), LT, smem_s, st>>>(P, items);
+    if (mode == 3) k_l21d<128, 4><<<dim3(nitems, batch), 512, 0, st>>>(P, items);
+    else if (mode == 1 && l21d_max() >= 64) k_l21d<64, 1><<<dim3(nitems, batch), 128, 0, st>>>(P, items);
+    else if (mode == 1) k_l21<1><<<dim3(nitems, batch), LT, smem_s, st>>>(P, items);
     else if (mode == 2) k_l21<2><<<dim3(nitems, batch), LT, smem, st>>>(P, items);
     else k_l21<0><<<dim3(nitems, batch), LT, smem, st>>>(P, items);
 }
 
 int l21_mode(int qcap) {
+    const int dm = l21d_max();
+    if (dm >= 64 && qcap <= 64) return 1;
+    if (dm >= 128 && qcap <= 128) return 3;
     if (qcap < LB) return 1;
     if (qcap >= kXMin && qcap <= (LB - 1) * kXMaxBlocks) return 2;
     return 0;

@@ -166,7 +166,7 @@ class InertiaInfo:
 class Kep:
     """One analysed pattern on one device (kep_ctx)."""
 
-    def __init__(self, n, colptr, rowidx, ordering="auto", user_perm=None, amalgamate=True, nrelax=16,
+    def __init__(self, n, colptr, rowidx, ordering="auto", user_perm=None, amalgamate=True, nrelax=48,
                  relax_frac=0.05, pivot_u=0.01, tau_sing=1e-14, delay_slack=16, max_batch=16, device=-1,
                  stream=None, kernel_variant=0, profile=False):
         L = lib()

@@ -35,9 +35,14 @@ def main():
     t = time.time()
     p, lo, hi = cached(cfg, shape)
     print(f"gen {time.time() - t:.1f}s n={p.n}", flush=True)
-    k = Kep.from_pencil(p, max_batch=m, profile=True)
+    kw = {}
+    if os.environ.get("KEP_NRELAX"):
+        kw["nrelax"] = int(os.environ["KEP_NRELAX"])
+    if os.environ.get("KEP_RELAX_FRAC"):
+        kw["relax_frac"] = float(os.environ["KEP_RELAX_FRAC"])
+    k = Kep.from_pencil(p, max_batch=m, profile=True, **kw)
     a = k.analysis()
-    print({x: a[x] for x in ("n_fronts", "n_levels", "max_front", "flops", "arena_bytes", "batch")}, flush=True)
+    print(kw, {x: a[x] for x in ("n_fronts", "n_levels", "max_front", "flops", "flops_exec", "arena_bytes", "batch")}, flush=True)
     k.set_values(p.a, p.b)
     sig = kepgen.uniform_shifts(lo, hi, m)
     k.inertia_many(sig)
