@@ -83,6 +83,7 @@ struct kep_ctx {
     int4* d_smitems = nullptr;                  // k_asm_smem strips (front, x, S, 0) per level
     std::vector<int64_t> smitem_off, smitem_cnt;
     std::vector<char> asm_red;                  // per level: small fronts, k_assemble_red
+    std::vector<int> level_fmax;                // per level: largest front capacity (k_assemble_red strips)
     std::vector<int64_t> fast_off, fast_cnt, ref_off, ref_cnt, item_off, item_cnt, litem_off, litem_cnt;
     // fast-path pivot records: per-front offsets (entries), per shift stride (doubles)
     int64_t* d_aux_off = nullptr;
@@ -347,6 +348,7 @@ kep_status build_lists(kep_ctx* c) {
     c->item_off.assign(nl, 0); c->item_cnt.assign(nl, 0);
     c->level_qmax.assign(nl, 0);
     c->asm_red.assign(nl, 0);
+    c->level_fmax.assign(nl, 0);
     c->fs_groups.clear();
     for (int L = 0; L < nl; ++L) {
         c->fast_off[L] = (int64_t)fast.size();
@@ -366,6 +368,8 @@ kep_status build_lists(kep_ctx* c) {
             for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) sf += S.forder[S.level_fronts[k]];
             const int nlf = S.level_ptr[L + 1] - S.level_ptr[L];
             c->asm_red[L] = nlf > 0 && sf / nlf < 700.0;
+            for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k)
+                c->level_fmax[L] = std::max(c->level_fmax[L], (int)S.capacity[S.level_fronts[k]]);
         }
         for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) strips(S.level_fronts[k], INT_MAX);
         c->aitem_cnt[L] = (int64_t)aitems.size() - c->aitem_off[L];
@@ -404,7 +408,7 @@ kep_status build_lists(kep_ctx* c) {
                 kep_ctx::SmGroup g{(int64_t)smf.size(), 0, kCls[cl], kTh[cl]};
                 for (int k = S.level_ptr[L]; k < S.level_ptr[L + 1]; ++k) {
                     const int s = S.level_fronts[k];
-                    if (!is_small(s)) continue;
+                    if (!is_small(s) || is_big(s)) continue;     // a big front is factored by k_bigp only
                     const int64_t need = (int64_t)S.forder[s] * (S.npiv[s] + kSmallPlan);
                     if (need <= kCls[cl] && (cl == 0 || need > kCls[cl - 1])) smf.push_back(s);
                 }
@@ -898,7 +902,7 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
             cur_level = L;
             mark(KEP_K_ASSEMBLE, true);
             if (c->smitem_cnt[L]) kep::launch_asm_smem(P, c->d_smitems + c->smitem_off[L], (int)c->smitem_cnt[L], m, c->stream);
-            else if (c->asm_red[L]) kep::launch_assemble_red(P, c->d_level_fronts + b, nfl, m, c->stream);
+            else if (c->asm_red[L]) kep::launch_assemble_red(P, c->d_level_fronts + b, nfl, m, c->level_fmax[L], c->stream);
             else kep::launch_assemble(P, c->d_aitems + c->aitem_off[L], (int)c->aitem_cnt[L], m, false, c->stream);
             mark(KEP_K_ASSEMBLE, false);
             if (resid) kep::launch_capture(P, c->d_level_fronts + b, nfl, c->d_f0, c->stream);

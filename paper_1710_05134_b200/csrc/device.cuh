@@ -164,7 +164,7 @@ struct StorePlan {
 
 // Launchers (kernels.cu, kernels_front.cu, kernels_fast.cu, kernels_solve.cu)
 void launch_assemble(const DevPlan& P, const int4* items, int nitems, int batch, bool only_flagged, cudaStream_t st);
-void launch_assemble_red(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
+void launch_assemble_red(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int fmax, cudaStream_t st);
 int assembly_strips(int forder);     // CTAs (column strips) per front of the given order
 int smem_strips(int cap);            // k_asm_smem strips of a front of capacity cap (0: too large)
 void launch_asm_smem(const DevPlan& P, const int4* items, int nitems, int batch, cudaStream_t st);

@@ -480,10 +480,13 @@ __device__ __forceinline__ void assemble_front_red(const DevPlan& P, const int32
     __syncthreads();
     const double sigma = P.sigma[sh], alpha = P.alpha[sh];
     double mx = 0.0;
-    for (int64_t k = P.asm_ptr[s] + threadIdx.x; k < P.asm_ptr[s + 1]; k += kAsmRedThreads) {
+    // original entries of the strip's columns only (they sit in the pivot columns; asm_col: first
+    // entry of each local pivot column)
+    const int32_t* acol = P.asm_col + P.piv_first[s] + s;
+    const int64_t k0 = P.asm_ptr[s] + acol[min(clo, p)], k1 = P.asm_ptr[s] + acol[min(chi, p)];
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += kAsmRedThreads) {
         const uint32_t rc = P.asm_rc[k];
         const int lr = (int)(rc >> 16), lc = (int)(rc & 0xffffu);
-        if (lc < clo || lc >= chi) continue;
         const int r = lr < p ? lr : lr + nd;
         const double v = fma(-sigma, P.b[k], alpha * P.a[k]);      // alpha A - sigma B (alpha = 1: A - sigma B)
         F[r + (size_t)lc * ld] = v;
@@ -543,7 +546,8 @@ __device__ __forceinline__ void assemble_front_red(const DevPlan& P, const int32
                         const int hi = pi > pj ? pi : pj, lo = pi > pj ? pj : pi;
                         if (lo >= clo && lo < chi) {
                             dst[u] = hi + (size_t)lo * ld;
-                            v[u] = (wup && j < ndo && i >= ndo) ? Fc[(ec + j) + (size_t)(ec + i) * ldc] : colc[i];
+                            v[u] = (wup && j < ndo && i >= ndo) ? __ldcs(Fc + (ec + j) + (size_t)(ec + i) * ldc)
+                                                                : __ldcs(colc + i);   // read once: evict-first
                         }
                     }
                 }
@@ -967,9 +971,12 @@ int assembly_strips(int forder) {
     return (int)std::max<int64_t>(1, (T + kAsmStripEnt - 1) / kAsmStripEnt);
 }
 
-void launch_assemble_red(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+void launch_assemble_red(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int fmax, cudaStream_t st) {
     if (nfronts <= 0) return;
-    // CTAs per front: enough to give ~4 resident CTAs per SM on the whole level
+    // CTAs per front: enough to give ~4 resident CTAs per SM on the whole level (column strips of at
+    // most 64 KB for L2 residency between the zero fill and the RED adds were measured slower at c4:
+    // 8192 entries 122 ms, 16384 97 ms, whole fronts 95 ms per 8-shift batch)
+    (void)fmax;
     int S = (int)((4 * 148 + (int64_t)nfronts * batch - 1) / ((int64_t)nfronts * batch));
     S = std::max(1, std::min(S, 16));
     k_assemble_red<<<dim3(nfronts * S, batch), kAsmRedThreads, 0, st>>>(P, fronts, S);
