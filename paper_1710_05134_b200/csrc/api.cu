@@ -98,6 +98,7 @@ struct kep_ctx {
     int64_t gscratch_stride = 0;
     double* d_gscratch = nullptr;
     std::vector<int64_t> uitem_off, uitem_cnt, small_off, small_cnt;
+    std::vector<int> small_cmax, small_kmax;    // per level: largest CB order / pivot count of the k_schur_small fronts
     // k_small (whole FS panel in shared memory): per level list offsets, shared-memory cap, threads
     int32_t* d_smfronts = nullptr;
     struct SmGroup { int64_t off, cnt; int cap, th; };
@@ -343,6 +344,7 @@ kep_status build_lists(kep_ctx* c) {
     };
     c->uitem_off.assign(nl, 0); c->uitem_cnt.assign(nl, 0);
     c->small_off.assign(nl, 0); c->small_cnt.assign(nl, 0);
+    c->small_cmax.assign(nl, 0); c->small_kmax.assign(nl, 0);
     c->fast_off.assign(nl, 0); c->fast_cnt.assign(nl, 0);
     c->ref_off.assign(nl, 0); c->ref_cnt.assign(nl, 0);
     c->item_off.assign(nl, 0); c->item_cnt.assign(nl, 0);
@@ -448,6 +450,8 @@ kep_status build_lists(kep_ctx* c) {
                 const int qq = S.npiv[s] + kSmallDelay;
                 if (kep::schur_small_ok(S.ncb[s], qq)) {
                     small.push_back(s);
+                    c->small_cmax[L] = std::max(c->small_cmax[L], (int)S.ncb[s]);
+                    c->small_kmax[L] = std::max(c->small_kmax[L], qq);
                 } else {
                     const int nt = (S.ncb[s] + 63) / 64;
                     for (int I = 0; I < nt; ++I)
@@ -474,6 +478,8 @@ kep_status build_lists(kep_ctx* c) {
             rd1[s].z = (int)li.size() - rd1[s].y;
             if (kep::schur_small_ok(S.ncb[s], qcap)) {
                 small.push_back(s);                                  // whole CB in one CTA
+                c->small_cmax[L] = std::max(c->small_cmax[L], (int)S.ncb[s]);
+                c->small_kmax[L] = std::max(c->small_kmax[L], qcap);
             } else {
                 const int nt = (S.ncb[s] + 63) / 64;
                 for (int I = 0; I < nt; ++I)
@@ -1056,7 +1062,8 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 mark(cls, true);
                 if (tma) kep::launch_schur_tma(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
                 else kep::launch_schur(P, c->d_items + c->item_off[L], (int)c->item_cnt[L], m, c->stream);
-                kep::launch_schur_small(P, c->d_small + c->small_off[L], (int)c->small_cnt[L], m, c->stream);
+                kep::launch_schur_small(P, c->d_small + c->small_off[L], (int)c->small_cnt[L], m, c->small_cmax[L],
+                                        c->small_kmax[L], c->stream);
                 mark(cls, false);
                 c->prof.launches[cls] += (c->item_cnt[L] ? 1 : 0) + (c->small_cnt[L] ? 1 : 0);
                 c->prof.schur_flops += c->item_flops[L] * m;

@@ -216,7 +216,8 @@ void launch_schur_tma(const DevPlan& P, const int4* items, int nitems, int batch
 // host: encode the 2-D tensor map of one (arena base, leading dimension) pair (TMA box 16 x 64 doubles,
 // 128-byte swizzle); false if the driver entry point is unavailable
 bool encode_front_tmap(CUtensorMap* out, double* arena_base, int64_t arena_doubles, int ld);
-void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st);
+void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int cmax, int kmax,
+                        cudaStream_t st);
 bool schur_small_ok(int c, int qcap);     // front handled by k_schur_small
 void launch_factor_list(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st,
                         bool only_flagged = false);

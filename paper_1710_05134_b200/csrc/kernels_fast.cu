@@ -265,11 +265,12 @@ constexpr int SS_T = 256;
 constexpr int SS_C = 256;       // max CB order
 constexpr int SS_K = 48;        // max eliminated pivots
 constexpr int SS_P = SS_K + 4;  // = 4 (mod 16)
+constexpr int SS_QMAX = 128;   // eliminated pivots at most (k_small's FS limit)
 
 template <bool RED>
-__global__ void __launch_bounds__(SS_T) k_schur_small(DevPlan P, const int32_t* __restrict__ fronts) {
-    extern __shared__ __align__(16) double Gs[];        // [SS_C][SS_P]
-    __shared__ unsigned long long Sg[SS_K];
+__global__ void __launch_bounds__(SS_T) k_schur_small(DevPlan P, const int32_t* __restrict__ fronts, int SP) {
+    extern __shared__ __align__(16) double Gs[];        // [c][SP], SP = 4 (mod 16) >= K4 of the level's fronts
+    __shared__ unsigned long long Sg[SS_QMAX];
     const int s = fronts[blockIdx.x];
     const int sh = blockIdx.y;
     const int nd = P.nd_in[(size_t)sh * P.nf + s];
@@ -279,66 +280,73 @@ __global__ void __launch_bounds__(SS_T) k_schur_small(DevPlan P, const int32_t* 
     const int p = P.npiv[s], c = P.ncb[s];
     const int f = P.forder[s] + nd, q = p + nd, ld = ldpad(P.cap[s]);
     const int e = q - ndo;
-    if (e <= 0 || c <= 0) return;
+    if (e <= 0 || c <= 0 || e > SS_QMAX) return;       // (e <= 128: k_small's limit; FS capacity <= SS_K otherwise)
     double* F = P.arena + (size_t)sh * P.arena_stride + P.arena_off[s];
     const AuxRec A = aux_rec(P, sh, s, P.cap[s] - c);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, tg = lane & 3;
     const int K4 = (e + 3) & ~3;
-    for (int x = tid; x < c * K4; x += SS_T) {            // G rows of the CB (upper part), zero-padded to K4
-        const int i = x / K4, t = x - i * K4;
-        const bool v = t < e;
-        cp_async8(&Gs[i * SS_P + t], F + (v ? (t + (size_t)(q + i) * ld) : 0), v);
-    }
-    cp_async_commit();
-    if (tid < SS_K) Sg[tid] = (tid < e && A.sgn[tid] < 0.0) ? 0x8000000000000000ull : 0ull;
-    cp_async_wait<0>();
-    __syncthreads();
+    // K chunk held in shared memory: one chunk unless a k_small front received more delayed columns
+    // than its plan (its pivot count can then exceed the level's planned maximum)
+    const int KW = SP - 4;
+    for (int t = tid; t < SS_QMAX; t += SS_T) Sg[t] = (t < e && A.sgn[t] < 0.0) ? 0x8000000000000000ull : 0ull;
     const int T = (c + 31) >> 5;
     const int ntile = T * (T + 1) / 2;
-    for (int tile = warp; tile < ntile; tile += SS_T / 32) {
-        int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
-        while ((I + 1) * (I + 2) / 2 <= tile) ++I;
-        while (I * (I + 1) / 2 > tile) --I;
-        const int J = tile - I * (I + 1) / 2;
-        const int i0 = 32 * I, j0 = 32 * J;
-        double acc[4][4][2];
+    for (int kc0 = 0; kc0 < K4; kc0 += KW) {
+        const int kw = min(KW, K4 - kc0);
+        __syncthreads();                                 // previous chunk consumed (and Sg written)
+        for (int x = tid; x < c * kw; x += SS_T) {       // G rows of the CB (upper part), zero-padded to K4
+            const int i = x / kw, t = x - i * kw;
+            const bool v = kc0 + t < e;
+            cp_async8(&Gs[i * SP + t], F + (v ? (kc0 + t + (size_t)(q + i) * ld) : 0), v);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        for (int tile = warp; tile < ntile; tile += SS_T / 32) {
+            int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+            while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+            while (I * (I + 1) / 2 > tile) --I;
+            const int J = tile - I * (I + 1) / 2;
+            const int i0 = 32 * I, j0 = 32 * J;
+            double acc[4][4][2];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-        for (int k4 = 0; k4 < K4; k4 += 4) {
-            double a[4], b[4];
-            const long long sm = (long long)Sg[k4 + tg];
+                for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+            for (int k4 = 0; k4 < kw; k4 += 4) {
+                double a[4], b[4];
+                const long long sm = (long long)Sg[kc0 + k4 + tg];
 #pragma unroll
-            for (int mb = 0; mb < 4; ++mb) {
-                const int i = i0 + 8 * mb + g;
-                a[mb] = i < c ? Gs[i * SS_P + k4 + tg] : 0.0;
-            }
+                for (int mb = 0; mb < 4; ++mb) {
+                    const int i = i0 + 8 * mb + g;
+                    a[mb] = i < c ? Gs[i * SP + k4 + tg] : 0.0;
+                }
 #pragma unroll
-            for (int nb = 0; nb < 4; ++nb) {
-                const int j = j0 + 8 * nb + g;
-                b[nb] = j < c ? __longlong_as_double(__double_as_longlong(Gs[j * SS_P + k4 + tg]) ^ sm) : 0.0;
+                for (int nb = 0; nb < 4; ++nb) {
+                    const int j = j0 + 8 * nb + g;
+                    b[nb] = j < c ? __longlong_as_double(__double_as_longlong(Gs[j * SP + k4 + tg]) ^ sm) : 0.0;
+                }
+#pragma unroll
+                for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb], a[mb], b[nb]);
             }
 #pragma unroll
             for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
-                for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb], a[mb], b[nb]);
-        }
+                for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-        for (int mb = 0; mb < 4; ++mb)
-#pragma unroll
-            for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int i = i0 + 8 * mb + g;
-                    const int j = j0 + 8 * nb + 2 * tg + h;
-                    if (i < c && j < c && i >= j) {
-                        double* x = &F[(q + i) + (size_t)(q + j) * ld];
-                        if (RED) atomicAdd(x, -acc[mb][nb][h]);
-                        else *x -= acc[mb][nb][h];                     // the tile's only writer
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = i0 + 8 * mb + g;
+                        const int j = j0 + 8 * nb + 2 * tg + h;
+                        if (i < c && j < c && i >= j) {
+                            double* x = &F[(q + i) + (size_t)(q + j) * ld];
+                            if (RED) atomicAdd(x, -acc[mb][nb][h]);
+                            else *x -= acc[mb][nb][h];                     // the tile's only writer
+                        }
                     }
-                }
+        }
     }
 }
 
@@ -384,16 +392,20 @@ bool encode_front_tmap(CUtensorMap* out, double* base, int64_t arena_doubles, in
 
 bool schur_small_ok(int c, int qcap) { return c > 0 && c <= SS_C && qcap <= SS_K; }
 
-void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, cudaStream_t st) {
+void launch_schur_small(const DevPlan& P, const int32_t* fronts, int nfronts, int batch, int cmax, int kmax,
+                        cudaStream_t st) {
     if (nfronts <= 0) return;
-    const size_t smem = sizeof(double) * SS_C * SS_P;
+    // shared memory sized for the level's largest CB and planned pivot count, not the kernel maxima
+    const int SP = ((((kmax + 3) & ~3) + 15) & ~15) + 4;       // >= K4, = 4 (mod 16)
+    const size_t smem = sizeof(double) * (size_t)std::min(cmax, SS_C) * SP;
+    const size_t smax = sizeof(double) * SS_C * SS_P;           // the opt-in covers every level
     static unsigned long long attr = 0;
     if (first_on_device(attr)) {
-        cudaFuncSetAttribute(k_schur_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_schur_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_schur_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+        cudaFuncSetAttribute(k_schur_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
     }
     static const bool red = getenv("KEP_SCHUR_NORED") == nullptr;   // RED measured 2.6x faster at c4 level 0
-    if (red) k_schur_small<true><<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts);
-    else k_schur_small<false><<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts);
+    if (red) k_schur_small<true><<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts, SP);
+    else k_schur_small<false><<<dim3(nfronts, batch), SS_T, smem, st>>>(P, fronts, SP);
 }
 }  // namespace kep

@@ -1336,7 +1336,9 @@ void launch_fsp(const DevPlan& P, const int32_t* fronts, int nfronts, int batch,
     const size_t smem = fs_smem_bytes(nb, RS, gls);
     if (gls) return launch_fsp_t<16, 256, true>(P, fronts, nfronts, batch, RS, smem, mode, st);
     // threads per front: one warp for tiny FS blocks (no CTA-wide barriers), 4 or 8 warps above
-    const int th = qmax <= 40 ? 32 : (qmax <= 192 ? 128 : 256);
+    static const int q1 = [] { const char* x = getenv("KEP_FSP_Q1"); return x ? atoi(x) : 40; }();
+    static const int q4 = [] { const char* x = getenv("KEP_FSP_Q4"); return x ? atoi(x) : 192; }();
+    const int th = qmax <= q1 ? 32 : (qmax <= q4 ? 128 : 256);
 #define KEP_FSP(NBV, THV) if (nb == NBV && th == THV) return launch_fsp_t<NBV, THV, false>(P, fronts, nfronts, batch, RS, smem, mode, st)
     KEP_FSP(32, 32); KEP_FSP(32, 128); KEP_FSP(32, 256);
     KEP_FSP(16, 32); KEP_FSP(16, 128); KEP_FSP(16, 256);
