@@ -76,7 +76,11 @@ struct kep_ctx {
     double* d_xscr = nullptr;
     int64_t xstride = 0;
     std::vector<int64_t> lsitem_off, lsitem_cnt, lxitem_off, lxitem_cnt, lditem_off, lditem_cnt, xfront_off, xfront_cnt;
-    struct FsGroup { int64_t foff, fcnt, uoff, ucnt; int qmax; };
+    struct FsGroup {
+        int64_t foff, fcnt, uoff, ucnt; int qmax;
+        int64_t loff[4], lcnt[4];                  // the group's range of each k_l21 mode list (mode 0, 1, 2, 3)
+        int64_t xoff, xcnt;                        // ... and of the level's k_l21x_prep fronts
+    };
     std::vector<std::vector<FsGroup>> fs_groups;   // per level: fast fronts by FS capacity (k_fsp/k_fsu passes)
     int4* d_aitems = nullptr;                   // k_assemble strips (front, x, S, 0): all fronts, then fast fronts
     std::vector<int64_t> aitem_off, aitem_cnt, raitem_off, raitem_cnt;
@@ -131,6 +135,10 @@ struct kep_ctx {
     // profiling
     kep_profile prof;
     std::vector<cudaEvent_t> ev_pool;
+    // FS-size groups of a level are disjoint front sets: groups 1.. run on forked streams so their
+    // latency-bound k_fsp/k_fsu chains overlap (KEP_FS_STREAMS=0: one stream)
+    cudaStream_t fs_streams[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t fs_fork = nullptr, fs_join[3] = {nullptr, nullptr, nullptr};
     std::vector<int> ev_class;
     std::vector<int> ev_level;
     std::vector<std::array<double, KEP_K_NCLASS>> lvl_ms;    // KEP_PROFILE_LEVELS: per level and class
@@ -465,17 +473,6 @@ kep_status build_lists(kep_ctx* c) {
                 continue;
             }
             c->level_qmax[L] = std::max(c->level_qmax[L], qcap);
-            const int lmode = kep::l21_mode(qcap);
-            auto& li = lmode == 1 ? lsitems : (lmode == 2 ? lxitems : (lmode == 3 ? lditems : litems));
-            if (lmode == 2) {
-                xfronts.push_back(s);
-                xoff[s] = xacc;
-                xacc += kep::l21_x_doubles(qcap);
-            }
-            rd1[s].x = lmode;
-            rd1[s].y = (int)li.size();
-            for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) li.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
-            rd1[s].z = (int)li.size() - rd1[s].y;
             if (kep::schur_small_ok(S.ncb[s], qcap)) {
                 small.push_back(s);                                  // whole CB in one CTA
                 c->small_cmax[L] = std::max(c->small_cmax[L], (int)S.ncb[s]);
@@ -497,6 +494,20 @@ kep_status build_lists(kep_ctx* c) {
             const int qcap = S.capacity[s] - S.ncb[s];
             if (!is_fast(s)) continue;
             fast.push_back(s);
+            {   // k_l21 row strips, in the same (sorted) order: a size group owns a contiguous range of
+                // each mode's list, so its k_fsp -> k_l21 chain can run on the group's stream
+                const int lmode = kep::l21_mode(qcap);
+                auto& li = lmode == 1 ? lsitems : (lmode == 2 ? lxitems : (lmode == 3 ? lditems : litems));
+                if (lmode == 2) {
+                    xfronts.push_back(s);
+                    xoff[s] = xacc;
+                    xacc += kep::l21_x_doubles(qcap);
+                }
+                rd1[s].x = lmode;
+                rd1[s].y = (int)li.size();
+                for (int I = 0; I < (S.ncb[s] + 127) / 128; ++I) li.push_back(make_int4(s, I, 0, 0));   // k_l21: 128 CB rows
+                rd1[s].z = (int)li.size() - rd1[s].y;
+            }
             fu.push_back((int64_t)uitems.size());
             rd1[s].w = (int)uitems.size();
             for (int I = 0; I < (qcap + 63) / 64; ++I)
@@ -526,11 +537,30 @@ kep_status build_lists(kep_ctx* c) {
                 }
             }
             std::vector<kep_ctx::FsGroup> gs;
-            const int64_t bnd[4] = {0, b1, b2, n};
-            for (int k2 = 0; k2 < 3; ++k2)
-                if (bnd[k2 + 1] > bnd[k2])
-                    gs.push_back({f0 + bnd[k2], bnd[k2 + 1] - bnd[k2], fu[bnd[k2]], fu[bnd[k2 + 1]] - fu[bnd[k2]],
-                                  (int)qc(bnd[k2 + 1] - 1)});
+            std::vector<int64_t> bnd = {0, b1, b2, n};
+            bnd.erase(std::unique(bnd.begin(), bnd.end()), bnd.end());
+            // a level left with one group is cut into KEP_FS_SPLIT (default 2) equal parts, so that on
+            // the forked streams one part's k_l21 (DMMA) overlaps another part's k_fsp (latency-bound);
+            // measured at c4 per 8 shifts: one stream 500.1 ms, forked 492.3, split 2/3/4: 489.0/493.0/493.5
+            static const int fs_split = [] { const char* x = getenv("KEP_FS_SPLIT"); return x ? atoi(x) : 2; }();
+            if (bnd.size() == 2 && fs_split > 1 && n >= 2 * fs_split) {
+                bnd.clear();
+                for (int k2 = 0; k2 <= std::min(fs_split, 4); ++k2) bnd.push_back(n * k2 / std::min(fs_split, 4));
+            }
+            for (size_t k2 = 0; k2 + 1 < bnd.size(); ++k2)
+                if (bnd[k2 + 1] > bnd[k2]) {
+                    kep_ctx::FsGroup g{f0 + bnd[k2], bnd[k2 + 1] - bnd[k2], fu[bnd[k2]], fu[bnd[k2 + 1]] - fu[bnd[k2]],
+                                       (int)qc(bnd[k2 + 1] - 1), {-1, -1, -1, -1}, {0, 0, 0, 0}, -1, 0};
+                    int64_t xi = c->xfront_off[L];               // xfronts index of the level's mode-2 fronts, in order
+                    for (int64_t x = 0; x < bnd[k2]; ++x) xi += rd1[fast[f0 + x]].x == 2;
+                    for (int64_t x = bnd[k2]; x < bnd[k2 + 1]; ++x) {
+                        const int4 r = rd1[fast[f0 + x]];
+                        if (g.loff[r.x] < 0) g.loff[r.x] = r.y;
+                        g.lcnt[r.x] += r.z;
+                        if (r.x == 2) { if (g.xoff < 0) g.xoff = xi; ++g.xcnt; ++xi; }
+                    }
+                    gs.push_back(g);
+                }
             c->fs_groups.push_back(gs);
         }
         c->ref_cnt[L] = (int64_t)ref.size() - c->ref_off[L];
@@ -964,23 +994,53 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 KEP_CUDA(c, cudaMemsetAsync(c->d_pending, 0, 2 * sizeof(int32_t), c->stream));
                 for (int pass = 0; pass <= kReruns; ++pass) {
                     if (pass == 0) {
-                        for (const auto& gr : groups) { // size groups of the level's fast fronts
+                        static const bool fs_fork_on = [] { const char* x = getenv("KEP_FS_STREAMS"); return !x || atoi(x) != 0; }();
+                        const bool forked = fs_fork_on && groups.size() > 1 && groups.size() <= 4;
+                        if (forked) {                   // groups 1.. on forked streams, joined before k_l21
+                            if (!c->fs_fork) {
+                                KEP_CUDA(c, cudaEventCreateWithFlags(&c->fs_fork, cudaEventDisableTiming));
+                                for (int x = 0; x < 3; ++x) {
+                                    KEP_CUDA(c, cudaStreamCreateWithFlags(&c->fs_streams[x], cudaStreamNonBlocking));
+                                    KEP_CUDA(c, cudaEventCreateWithFlags(&c->fs_join[x], cudaEventDisableTiming));
+                                }
+                            }
+                            mark(KEP_K_PANEL, true);    // one interval for the whole fork-join region
+                            KEP_CUDA(c, cudaEventRecord(c->fs_fork, c->stream));
+                        }
+                        for (size_t gi = 0; gi < groups.size(); ++gi) { // size groups of the level's fast fronts
+                            const auto& gr = groups[gi];
+                            cudaStream_t gst = (forked && gi > 0) ? c->fs_streams[gi - 1] : c->stream;
+                            if (forked && gi > 0) KEP_CUDA(c, cudaStreamWaitEvent(gst, c->fs_fork, 0));
                             const int64_t nbk = gr.fcnt * m;
                             const int iters = kep::fs_iters(gr.qmax, nbk);
                             for (int itn = 0; itn < iters; ++itn) {
-                                mark(KEP_K_PANEL, true);
-                                kep::launch_fsp(P, c->d_lists + gr.foff, (int)gr.fcnt, m, gr.qmax, itn == 0 ? 0 : 2, c->stream);
-                                mark(KEP_K_PANEL, false);
+                                if (!forked) mark(KEP_K_PANEL, true);
+                                kep::launch_fsp(P, c->d_lists + gr.foff, (int)gr.fcnt, m, gr.qmax, itn == 0 ? 0 : 2, gst);
+                                if (!forked) mark(KEP_K_PANEL, false);
                                 c->prof.launches[KEP_K_PANEL]++;
                                 if (gr.ucnt) {
-                                    mark(KEP_K_FSU, true);
-                                    kep::launch_fsu(P, c->d_uitems + gr.uoff, (int)gr.ucnt, m, c->stream);
-                                    mark(KEP_K_FSU, false);
+                                    if (!forked) mark(KEP_K_FSU, true);
+                                    kep::launch_fsu(P, c->d_uitems + gr.uoff, (int)gr.ucnt, m, gst);
+                                    if (!forked) mark(KEP_K_FSU, false);
                                     c->prof.launches[KEP_K_FSU]++;
                                 }
                             }
+                            if (forked) {               // the group's k_l21 launches follow on its stream
+                                if (gr.xcnt) kep::launch_l21x_prep(P, c->d_xfronts + gr.xoff, (int)gr.xcnt, m, gst);
+                                if (gr.lcnt[2]) kep::launch_l21(P, c->d_lxitems + gr.loff[2], (int)gr.lcnt[2], m, 2, gst);
+                                if (gr.lcnt[0]) kep::launch_l21(P, c->d_litems + gr.loff[0], (int)gr.lcnt[0], m, 0, gst);
+                                if (gr.lcnt[1]) kep::launch_l21(P, c->d_lsitems + gr.loff[1], (int)gr.lcnt[1], m, 1, gst);
+                                if (gr.lcnt[3]) kep::launch_l21(P, c->d_lditems + gr.loff[3], (int)gr.lcnt[3], m, 3, gst);
+                                c->prof.launches[KEP_K_L21] += (gr.xcnt > 0) + (gr.lcnt[0] > 0) + (gr.lcnt[1] > 0) +
+                                                               (gr.lcnt[2] > 0) + (gr.lcnt[3] > 0);
+                            }
+                            if (forked && gi > 0) {
+                                KEP_CUDA(c, cudaEventRecord(c->fs_join[gi - 1], gst));
+                                KEP_CUDA(c, cudaStreamWaitEvent(c->stream, c->fs_join[gi - 1], 0));
+                            }
                         }
-                        if (c->litem_cnt[L] || c->lsitem_cnt[L] || c->lxitem_cnt[L] || c->lditem_cnt[L]) {
+                        if (forked) mark(KEP_K_PANEL, false);
+                        if (!forked && (c->litem_cnt[L] || c->lsitem_cnt[L] || c->lxitem_cnt[L] || c->lditem_cnt[L])) {
                             mark(KEP_K_L21, true);
                             kep::launch_l21x_prep(P, c->d_xfronts + c->xfront_off[L], (int)c->xfront_cnt[L], m, c->stream);
                             kep::launch_l21(P, c->d_lxitems + c->lxitem_off[L], (int)c->lxitem_cnt[L], m, 2, c->stream);
@@ -2033,6 +2093,11 @@ void kep_destroy(kep_ctx* c) {
                         c->d_big_state, c->d_big_bars, c->d_smitems};
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
+        if (c->fs_fork) cudaEventDestroy(c->fs_fork);
+        for (int x = 0; x < 3; ++x) {
+            if (c->fs_join[x]) cudaEventDestroy(c->fs_join[x]);
+            if (c->fs_streams[x]) cudaStreamDestroy(c->fs_streams[x]);
+        }
         if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     }
     delete c;
