@@ -256,6 +256,7 @@ def main():
     ap.add_argument("--shape", default=None, help="override lattice, e.g. 10x10x400 (development only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-bracket", action="store_true", help="skip the time_to_bracket leg (ncu launch lists)")
     ap.add_argument("--cpu-length", type=int, default=150, help="sub-wire length of the cpu_baseline sample")
     ap.add_argument("--ref-length", type=int, default=100, help="sub-wire length of the reference-arm sample")
     ap.add_argument("--cpu-full", action="store_true",
@@ -402,19 +403,21 @@ def main():
                "h2d_bytes_per_step": int(2 * nnz * 8 + S * 8), "d2h_bytes_per_step": int(S * 8)}
 
     # ---- time to bracket: one complete stage 2 from the initial interval
-    if world > 1:
+    to_bracket = None
+    if not args.no_bracket:
+      if world > 1:
         dist.barrier()
-    torch.cuda.synchronize()
-    b2b0, b2b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    b2b0.record()
-    ms.trace.clear()
-    fin = ms.run(initial)
-    b2b1.record()
-    torch.cuda.synchronize()
-    tb = torch.tensor([b2b0.elapsed_time(b2b1) / 1e3], dtype=torch.float64, device=dev)
-    if world > 1:
+      torch.cuda.synchronize()
+      b2b0, b2b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+      b2b0.record()
+      ms.trace.clear()
+      fin = ms.run(initial)
+      b2b1.record()
+      torch.cuda.synchronize()
+      tb = torch.tensor([b2b0.elapsed_time(b2b1) / 1e3], dtype=torch.float64, device=dev)
+      if world > 1:
         dist.all_reduce(tb, op=dist.ReduceOp.MAX)
-    to_bracket = {"seconds": float(tb.item()), "rounds": len(ms.trace), "shifts_per_round": P,
+      to_bracket = {"seconds": float(tb.item()), "rounds": len(ms.trace), "shifts_per_round": P,
                   "k": meta["k"], "bracket": [fin.lo, fin.hi, fin.nu_lo, fin.nu_hi],
                   "table5_analogue": [{"interval": list(r.bracket[:2]), "index_range": list(r.bracket[2:]),
                                        "m": r.bracket[3] - r.bracket[2]} for r in ms.trace]}
@@ -444,6 +447,9 @@ def main():
                                   "frac": (prof["schur_tma_flops"] / tma_t / 1e12 / peak) if tma_t > 0 and peak > 0 else None,
                                   "share_of_schur_flops": prof["schur_tma_flops"] / max(prof["schur_flops"], 1.0)},
                 "kernel_ms": msd, "kernel_launches": prof["launches"], "dominant_by_time": dom,
+                "kernel_ms_note": "CUDA-event intervals per kernel class on the launching stream; on levels whose FS-size "
+                                  "groups run on forked streams the 'fs' interval spans the whole k_fsp/k_fsu/k_l21 "
+                                  "fork-join region (KEP_FS_STREAMS=0 separates the classes: profiles/r2_levels_c4.txt)",
                 "schur_flops_alg": prof["schur_flops"]}
         launches = int(sum(prof["launches"].values()) + prof["other_launches"])
         fac_tflops = ana["flops"] * shifts_total / t_max / world / 1e12
