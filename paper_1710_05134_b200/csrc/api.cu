@@ -137,8 +137,8 @@ struct kep_ctx {
     std::vector<cudaEvent_t> ev_pool;
     // FS-size groups of a level are disjoint front sets: groups 1.. run on forked streams so their
     // latency-bound k_fsp/k_fsu chains overlap (KEP_FS_STREAMS=0: one stream)
-    cudaStream_t fs_streams[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t fs_fork = nullptr, fs_join[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t fs_streams[7] = {};
+    cudaEvent_t fs_fork = nullptr, fs_join[7] = {};
     std::vector<int> ev_class;
     std::vector<int> ev_level;
     std::vector<std::array<double, KEP_K_NCLASS>> lvl_ms;    // KEP_PROFILE_LEVELS: per level and class
@@ -546,6 +546,16 @@ kep_status build_lists(kep_ctx* c) {
             if (bnd.size() == 2 && fs_split > 1 && n >= 2 * fs_split) {
                 bnd.clear();
                 for (int k2 = 0; k2 <= std::min(fs_split, 4); ++k2) bnd.push_back(n * k2 / std::min(fs_split, 4));
+            }
+            static const bool fs_split_all = [] { const char* x = getenv("KEP_FS_SPLIT_ALL"); return x && atoi(x) != 0; }();
+            if (fs_split_all && bnd.size() > 2) {                  // tuning: every cost-model group cut in two
+                std::vector<int64_t> b2;
+                for (size_t k2 = 0; k2 + 1 < bnd.size(); ++k2) {
+                    b2.push_back(bnd[k2]);
+                    if (bnd[k2 + 1] - bnd[k2] >= 4) b2.push_back((bnd[k2] + bnd[k2 + 1]) / 2);
+                }
+                b2.push_back(n);
+                bnd = b2;
             }
             for (size_t k2 = 0; k2 + 1 < bnd.size(); ++k2)
                 if (bnd[k2 + 1] > bnd[k2]) {
@@ -995,11 +1005,11 @@ kep_status run_batch(kep_ctx* c, int m, const double* sigmas, kep_factorization*
                 for (int pass = 0; pass <= kReruns; ++pass) {
                     if (pass == 0) {
                         static const bool fs_fork_on = [] { const char* x = getenv("KEP_FS_STREAMS"); return !x || atoi(x) != 0; }();
-                        const bool forked = fs_fork_on && groups.size() > 1 && groups.size() <= 4;
+                        const bool forked = fs_fork_on && groups.size() > 1 && groups.size() <= 8;
                         if (forked) {                   // groups 1.. on forked streams, joined before k_l21
                             if (!c->fs_fork) {
                                 KEP_CUDA(c, cudaEventCreateWithFlags(&c->fs_fork, cudaEventDisableTiming));
-                                for (int x = 0; x < 3; ++x) {
+                                for (int x = 0; x < 7; ++x) {
                                     KEP_CUDA(c, cudaStreamCreateWithFlags(&c->fs_streams[x], cudaStreamNonBlocking));
                                     KEP_CUDA(c, cudaEventCreateWithFlags(&c->fs_join[x], cudaEventDisableTiming));
                                 }
@@ -2094,7 +2104,7 @@ void kep_destroy(kep_ctx* c) {
         for (void* p : ptrs) cudaFree(p);
         for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
         if (c->fs_fork) cudaEventDestroy(c->fs_fork);
-        for (int x = 0; x < 3; ++x) {
+        for (int x = 0; x < 7; ++x) {
             if (c->fs_join[x]) cudaEventDestroy(c->fs_join[x]);
             if (c->fs_streams[x]) cudaStreamDestroy(c->fs_streams[x]);
         }
